@@ -1,0 +1,131 @@
+"""Oracle: DTLZ1-7 (restates ``temo/problems.py``) and LSMOP1 (self-oracle). Test infrastructure only.
+
+DTLZ parity vs the reference is by tolerance (1e-5 rel, BASELINE north star):
+NumPy's vectorised cos/sin/pow and CUDA's differ in the last ulp.
+
+LSMOP1 has no reference implementation (problems.py:18): this is a
+NumPy restatement of the standard definition (Cheng et al. 2017, cited at
+PAPER.md:518) in the PlatEMO formulation -- *parity unpinned*.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+DTLZ = ("dtlz1", "dtlz2", "dtlz3", "dtlz4", "dtlz5", "dtlz6", "dtlz7")
+
+
+def _rastrigin_g(xm):
+    """problems.py:69-71."""
+    z = xm - 0.5
+    return 100.0 * (xm.shape[1] + np.sum(z * z - np.cos(20.0 * np.pi * z), axis=1))
+
+
+def _sphere_g(xm):
+    """problems.py:74-76."""
+    z = xm - 0.5
+    return np.sum(z * z, axis=1)
+
+
+def _linear_front(pos, g, scale=0.5):
+    """problems.py:79-89 (scale 0.5 for DTLZ1)."""
+    n, m1 = pos.shape
+    m = m1 + 1
+    out = np.empty((n, m))
+    for i in range(m):
+        p = np.prod(pos[:, : m - 1 - i], axis=1)
+        if i:
+            p = p * (1.0 - pos[:, m - 1 - i])
+        out[:, i] = scale * (1.0 + g) * p
+    return out
+
+
+def _sphere_front(theta, g):
+    """problems.py:92-102."""
+    n, m1 = theta.shape
+    m = m1 + 1
+    out = np.empty((n, m))
+    for i in range(m):
+        p = np.prod(np.cos(theta[:, : m - 1 - i]), axis=1)
+        if i:
+            p = p * np.sin(theta[:, m - 1 - i])
+        out[:, i] = (1.0 + g) * p
+    return out
+
+
+def evaluate_dtlz(name, X, m):
+    """problems.py:105-136."""
+    X = np.asarray(X, dtype=np.float64)
+    pos, xm = X[:, : m - 1], X[:, m - 1:]
+    if name == "dtlz1":
+        return _linear_front(pos, _rastrigin_g(xm))
+    if name == "dtlz2":
+        return _sphere_front(pos * (np.pi / 2.0), _sphere_g(xm))
+    if name == "dtlz3":
+        return _sphere_front(pos * (np.pi / 2.0), _rastrigin_g(xm))
+    if name == "dtlz4":
+        return _sphere_front(np.power(pos, 100.0) * (np.pi / 2.0), _sphere_g(xm))
+    if name in ("dtlz5", "dtlz6"):
+        g = _sphere_g(xm) if name == "dtlz5" else np.sum(np.power(xm, 0.1), axis=1)
+        theta = np.empty_like(pos)
+        theta[:, 0] = pos[:, 0] * (np.pi / 2.0)
+        if m > 2:
+            bend = np.pi / (4.0 * (1.0 + g))[:, None]
+            theta[:, 1:] = bend * (1.0 + 2.0 * g[:, None] * pos[:, 1:])
+        return _sphere_front(theta, g)
+    if name == "dtlz7":
+        k = X.shape[1] - m + 1
+        g = 1.0 + 9.0 / k * np.sum(xm, axis=1)
+        out = np.empty((X.shape[0], m))
+        out[:, : m - 1] = pos
+        h = m - np.sum(pos / (1.0 + g)[:, None] * (1.0 + np.sin(3.0 * np.pi * pos)), axis=1)
+        out[:, m - 1] = (1.0 + g) * h
+        return out
+    raise ValueError(name)
+
+
+def lsmop_groups(m, d, nk=5):
+    """Chaotic subcomponent sizes: c_{j+1} = 3.8 c_j (1 - c_j), c_1 = 3.8*0.1*0.9.
+
+    Returns (sublen[m], offset[m+1]) where objective i's nk segments start at
+    column (m-1) + offset[i] + j*sublen[i].
+    """
+    c = [3.8 * 0.1 * (1.0 - 0.1)]
+    for _ in range(m - 1):
+        c.append(3.8 * c[-1] * (1.0 - c[-1]))
+    c = np.asarray(c)
+    sublen = np.floor(c / c.sum() * (d - m + 1) / nk).astype(np.int64)
+    offset = np.concatenate([[0], np.cumsum(sublen * nk)])
+    return sublen, offset
+
+
+def lsmop_bounds(m, d):
+    lower = np.zeros(d)
+    upper = np.concatenate([np.ones(m - 1), np.full(d - m + 1, 10.0)])
+    return lower, upper
+
+
+def evaluate_lsmop1(X, m, nk=5):
+    """LSMOP1: linear linkage, Sphere g on every group, linear (DTLZ1-type) front."""
+    X = np.asarray(X, dtype=np.float64)
+    n, d = X.shape
+    sublen, offset = lsmop_groups(m, d, nk)
+    idx = np.arange(m, d + 1, dtype=np.float64)  # 1-based indices of x^s
+    xs = (1.0 + idx / d) * X[:, m - 1:] - 10.0 * X[:, :1]
+    G = np.zeros((n, m))
+    for i in range(m):
+        for j in range(nk):
+            a = offset[i] + j * sublen[i]
+            seg = xs[:, a:a + sublen[i]]
+            G[:, i] = G[:, i] + np.sum(seg * seg, axis=1)
+    G = G / sublen / nk
+    ones = np.ones((n, 1))
+    head = np.cumprod(np.concatenate([ones, X[:, : m - 1]], axis=1), axis=1)[:, ::-1]
+    tail = np.concatenate([ones, 1.0 - X[:, m - 2::-1]], axis=1) if m > 1 else ones
+    return (1.0 + G) * head * tail
+
+
+def evaluate(name, X, m):
+    if name == "lsmop1":
+        return evaluate_lsmop1(X, m)
+    return evaluate_dtlz(name, X, m)
