@@ -1,0 +1,81 @@
+/*
+ * temo_b200 -- C ABI of the B200-native tensorized EMO selection hot path.
+ *
+ * Drop-in boundary for the reference package `temo` 0.1.0
+ * (/root/reference/pkg/src/temo).  The reference is pure Python/NumPy and has
+ * no FFI of its own; every entry point below replaces one NumPy stage and is
+ * bound from Python with ctypes (paper_2503_20286_b200/_lib.py; the stub a
+ * maintainer adds on the reference side is in INTEGRATION.md).
+ *
+ * Conventions (all entry points):
+ *   - device pointers, int64 sizes, row-major C-contiguous float64 matrices;
+ *   - `stream` is a cudaStream_t; work is enqueued, never synchronised;
+ *   - `ws`/`ws_bytes` is caller-provided device workspace (size from the
+ *     matching *_ws_bytes query); the library allocates nothing;
+ *   - return value: TEMO_OK or a host-side error (bad arguments, short
+ *     workspace, launch failure);
+ *   - `status` (device int32, may be NULL) receives TEMO_ST_* bits for
+ *     data-dependent errors detected on the device (NaN input, peel failure,
+ *     count repair failure) -- read it after the stream completes.  The Python
+ *     layer maps them to the reference's ValueError / RuntimeError.
+ */
+#ifndef TEMO_B200_H
+#define TEMO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *temo_stream_t; /* == cudaStream_t */
+
+/* host-side return codes */
+#define TEMO_OK 0
+#define TEMO_EINVAL 1     /* ValueError in the reference */
+#define TEMO_ENAN 2       /* ValueError (NaN objectives) */
+#define TEMO_ERUNTIME 3   /* RuntimeError */
+#define TEMO_EWORKSPACE 4 /* workspace too small */
+#define TEMO_ECUDA 5      /* CUDA launch/runtime failure */
+
+/* device-side status bits */
+#define TEMO_ST_NAN 1     /* ndsort.py:35-36  NaN objective -> ValueError */
+#define TEMO_ST_PEEL 2    /* ndsort.py:64-65  peeling did not terminate -> RuntimeError */
+#define TEMO_ST_FILL 4    /* nsga3.py:176-177 not enough last-front rows -> RuntimeError */
+#define TEMO_ST_DEMOTE 8  /* nsga3.py:180-181 demotion exceeds promotions -> RuntimeError */
+#define TEMO_ST_COUNT 16  /* nsga3.py:216-217 selection size mismatch -> RuntimeError */
+#define TEMO_ST_KRANGE 32 /* hype.py:43-44 / 68-69 k out of range -> ValueError */
+
+int temo_abi_version(void);
+const char *temo_strerror(int code);
+
+/* ---------------------------------------------------------------- ND sort
+ * Replaces ndsort.rank_assign (ndsort.py:47-71) and the dominance-matrix
+ * construction it relies on (ndsort.py:25-44).
+ *   F      : N x m float64 objectives (no NaN), 1 <= m <= 16, 1 <= N <= 2^20
+ *   n      : 1 <= n <= N; l_out receives sort(r)[n-1]
+ *   mode   : TEMO_RANK_SORT ranks every row (rank_assign semantics);
+ *            TEMO_RANK_SELECT stops once >= n rows are ranked and gives every
+ *            remaining row rank l+1 (exact for NSGA-III/HypE)
+ *   rank   : N int32 outputs
+ *   nfronts: (may be NULL) device int32, number of fronts peeled
+ */
+#define TEMO_RANK_SORT 0
+#define TEMO_RANK_SELECT 1
+size_t temo_rank_ws_bytes(int64_t N, int m);
+int temo_rank(const double *F, int64_t N, int m, int64_t n, int mode, int32_t *rank,
+              int32_t *l_out, int32_t *nfronts, int32_t *status, void *ws, size_t ws_bytes,
+              temo_stream_t stream);
+
+/* Dominance bitmap only (ndsort.dominance_matrix, ndsort.py:25-44):
+ * D_out is N x ceil(N/32) uint32 words, bit (j%32) of word [i][j/32] set iff
+ * row i dominates row j.  For parity tests at small N. */
+size_t temo_dominance_ws_bytes(int64_t N, int m);
+int temo_dominance(const double *F, int64_t N, int m, uint32_t *D_out, int32_t *status,
+                   void *ws, size_t ws_bytes, temo_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEMO_B200_H */

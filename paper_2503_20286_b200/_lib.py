@@ -1,0 +1,174 @@
+"""ctypes binding of the C ABI (``include/temo_b200.h``) and the host-side plumbing.
+
+PyTorch is used only for device memory, streams and (multi-GPU) process
+groups.  There is no CPU fallback: if ``libtemo_b200.so`` cannot be loaded or
+built, or no CUDA device is visible, every hot-path call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from . import build as _build
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int
+_SZ = ctypes.c_size_t
+_D = ctypes.c_double
+
+# name -> (restype, argtypes); must mirror include/temo_b200.h
+SIGNATURES = {
+    "temo_abi_version": (_I32, []),
+    "temo_strerror": (ctypes.c_char_p, [_I32]),
+    "temo_rank_ws_bytes": (_SZ, [_I64, _I32]),
+    "temo_rank": (_I32, [_P, _I64, _I32, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
+    "temo_dominance_ws_bytes": (_SZ, [_I64, _I32]),
+    "temo_dominance": (_I32, [_P, _I64, _I32, _P, _P, _P, _SZ, _P]),
+}
+
+TEMO_OK, TEMO_EINVAL, TEMO_ENAN, TEMO_ERUNTIME, TEMO_EWORKSPACE, TEMO_ECUDA = range(6)
+ST_NAN, ST_PEEL, ST_FILL, ST_DEMOTE, ST_COUNT, ST_KRANGE = 1, 2, 4, 8, 16, 32
+
+_lock = threading.Lock()
+_handle = None
+
+
+class TemoError(RuntimeError):
+    pass
+
+
+def lib_path() -> Path:
+    return _build.LIB
+
+
+def lib():
+    """Load (building first if the in-tree .so is missing or stale) the CUDA library."""
+    global _handle
+    if _handle is not None:
+        return _handle
+    with _lock:
+        if _handle is None:
+            path = _build.LIB
+            if not _build.up_to_date() and os.environ.get("TEMO_NO_BUILD") != "1":
+                _build.build()
+            if not path.exists():
+                raise TemoError(f"CUDA library missing: {path} (run __graft_entry__.build())")
+            h = ctypes.CDLL(str(path))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(h, name)
+                fn.restype = res
+                fn.argtypes = args
+            _handle = h
+    return _handle
+
+
+def check(rc: int, what: str):
+    if rc == TEMO_OK:
+        return
+    msg = lib().temo_strerror(rc).decode()
+    if rc in (TEMO_EINVAL, TEMO_ENAN):
+        raise ValueError(f"{what}: {msg}")
+    if rc == TEMO_ERUNTIME:
+        raise RuntimeError(f"{what}: {msg}")
+    raise TemoError(f"{what}: {msg} (code {rc})")
+
+
+def raise_status(bits: int, what: str):
+    """Map device status bits to the reference's exceptions."""
+    if not bits:
+        return
+    if bits & ST_NAN:
+        raise ValueError(f"{what}: objective matrix contains NaN rows")
+    if bits & ST_KRANGE:
+        raise ValueError(f"{what}: k out of range")
+    if bits & ST_PEEL:
+        raise RuntimeError(f"{what}: front peeling failed to terminate")
+    if bits & ST_FILL:
+        raise RuntimeError(f"{what}: not enough last-front rows to reach n")
+    if bits & ST_DEMOTE:
+        raise RuntimeError(f"{what}: cannot demote more rows than were promoted")
+    if bits & ST_COUNT:
+        raise RuntimeError(f"{what}: selection produced the wrong number of rows")
+    raise RuntimeError(f"{what}: device status {bits:#x}")
+
+
+# ------------------------------------------------------------------ torch plumbing
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def device(dev=None):
+    t = torch()
+    if not t.cuda.is_available():
+        raise TemoError("no CUDA device: the temo_b200 hot path has no CPU fallback")
+    if dev is None:
+        return t.device("cuda", t.cuda.current_device())
+    return t.device(dev)
+
+
+def stream_handle(dev=None):
+    t = torch()
+    return _P(t.cuda.current_stream(dev).cuda_stream)
+
+
+def ptr(x):
+    if x is None:
+        return None
+    return _P(x.data_ptr())
+
+
+class _Workspace:
+    """Per-device grow-only scratch buffer handed to the C ABI."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, nbytes: int, dev):
+        t = torch()
+        key = (str(dev), threading.get_ident())
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            self.bufs[key] = None
+            buf = t.empty(max(int(nbytes), 256), dtype=t.uint8, device=dev)
+            self.bufs[key] = buf
+        return buf
+
+    def release(self):
+        self.bufs.clear()
+
+
+workspace = _Workspace()
+
+
+def as_device(x, dtype, dev=None):
+    """numpy/tensor -> contiguous CUDA tensor of ``dtype``; returns (tensor, was_numpy)."""
+    t = torch()
+    if isinstance(x, t.Tensor):
+        d = x.device if x.is_cuda else device(dev)
+        return x.to(device=d, dtype=dtype).contiguous(), False
+    arr = np.ascontiguousarray(np.asarray(x), dtype=_np_dtype(dtype))
+    return t.from_numpy(arr).to(device(dev), non_blocking=False), True
+
+
+def _np_dtype(tdtype):
+    t = torch()
+    return {t.float64: np.float64, t.int64: np.int64, t.int32: np.int32,
+            t.uint8: np.uint8, t.uint32: np.uint32}[tdtype]
+
+
+def new_status(dev):
+    t = torch()
+    return t.zeros(1, dtype=t.int32, device=dev)
+
+
+def sync_status(status, what):
+    bits = int(status.item())
+    raise_status(bits, what)

@@ -1,0 +1,654 @@
+// Non-dominated sorting on B200 (replaces temo ndsort.py:25-71).
+//
+// Pipeline (all on one stream, no host round trip):
+//   K0  per-column dense ranks of the objectives (u32; -0.0 == +0.0), so every
+//       dominance compare becomes an integer ISETP;
+//       lexicographic sort of the rank tuples; run-start id for duplicate tuples.
+//       In lex order row i can only dominate rows j > i, and for i < j
+//           i dom j  <=>  id_i < id_j  &&  r_k(i) <= r_k(j)  for k = 1..m-1
+//       (column 0 is implied by the order), so D is strictly upper triangular.
+//   K1  k_dom_bits: 256x256 tiles of the upper triangle; lane = column j,
+//       loop over rows i staged in shared memory, warp ballot -> one 32-bit
+//       word of row i; rows written as a packed triangular bitmap (N^2/16 B).
+//   K2  k_peel: one cooperative persistent kernel.  Dominated-by counts are a
+//       vertical popcount of the bitmap (nibble-SWAR counters, coalesced 128 B
+//       row segments); each front is detected (count == 0, unranked),
+//       compacted in index order, and its rows' bits are subtracted from the
+//       counts, front after front, with grid-wide barriers instead of host
+//       round trips (ndsort.py:60-69).
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace temo {
+
+constexpr int TILE = 256;        // K1 tile edge (rows i and columns j)
+constexpr int CHUNK = 8;         // K1: row tiles per work item
+constexpr int PEEL_T = 256;      // K2 threads per CTA
+constexpr int ROWS_PER_WARP = 30;
+constexpr int LC = 8 * ROWS_PER_WARP;  // K2: list rows per work item (<= 255 per byte counter)
+constexpr int MAX_M = 16;
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+// ------------------------------------------------------------------ plan
+struct RankPlan {
+    int64_t N, Np, W, nT, NB;
+    int m, NV, bitsN;
+    size_t cub_bytes;
+    // buffers
+    uint64_t *keys_a, *keys_b;
+    int32_t *vals_a, *vals_b, *scan_a, *scan_b;
+    uint32_t *R;       // N x MP column ranks
+    uint4 *rec;        // Np x NV records in lex order
+    int64_t *rt_off;   // nT row-tile offsets into bits
+    uint32_t *bits;    // packed triangular bitmap
+    int32_t *cnt, *rank_s, *list, *blkcnt;
+    void *cub_tmp;
+    size_t total;
+};
+
+static int64_t bitmap_words(int64_t nT, int64_t W) {
+    // row tile I stores words [8I, W) for its 256 rows
+    return (int64_t)TILE * (nT * W - 8 * nT * (nT - 1) / 2);
+}
+
+static size_t cub_need(int64_t N) {
+    size_t a = 0, b = 0, c = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (int32_t *)nullptr, (int32_t *)nullptr, (int)N);
+    cub::DeviceScan::InclusiveSum(nullptr, b, (int32_t *)nullptr, (int32_t *)nullptr, (int)N);
+    cub::DeviceScan::InclusiveScan(nullptr, c, (int32_t *)nullptr, (int32_t *)nullptr,
+                                   cub::Max(), (int)N);
+    return a > b ? (a > c ? a : c) : (b > c ? b : c);
+}
+
+static void plan_rank(RankPlan &p, void *base, int64_t N, int m) {
+    p.N = N;
+    p.m = m;
+    p.Np = round_up(N, 1024);
+    p.W = p.Np / 32;
+    p.nT = p.Np / TILE;
+    p.NB = p.Np / 1024;
+    p.NV = (m + 3) / 4;
+    int b = 1;
+    while ((int64_t(1) << b) < N) ++b;
+    p.bitsN = b;
+    p.cub_bytes = cub_need(N);
+    Carve c(base);
+    p.keys_a = c.take<uint64_t>(N);
+    p.keys_b = c.take<uint64_t>(N);
+    p.vals_a = c.take<int32_t>(N);
+    p.vals_b = c.take<int32_t>(N);
+    p.scan_a = c.take<int32_t>(N);
+    p.scan_b = c.take<int32_t>(N);
+    p.R = c.take<uint32_t>((size_t)N * 4 * p.NV);
+    p.rec = c.take<uint4>((size_t)p.Np * p.NV);
+    p.rt_off = c.take<int64_t>(p.nT);
+    p.bits = c.take<uint32_t>((size_t)bitmap_words(p.nT, p.W));
+    p.cnt = c.take<int32_t>(p.Np);
+    p.rank_s = c.take<int32_t>(p.Np);
+    p.list = c.take<int32_t>(p.Np);
+    p.blkcnt = c.take<int32_t>(p.NB + 1);
+    p.cub_tmp = c.take<char>(p.cub_bytes);
+    p.total = c.off;
+}
+
+// ------------------------------------------------------------------ K0
+__global__ void k_col_keys(const double *__restrict__ F, int64_t N, int m, int col,
+                           uint64_t *__restrict__ keys, int32_t *__restrict__ vals,
+                           int32_t *status) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    double x = F[i * m + col];
+    if (isnan(x)) flag_status(status, TEMO_ST_NAN);
+    keys[i] = ordered_key(x);
+    vals[i] = (int32_t)i;
+}
+
+__global__ void k_key_change(const uint64_t *__restrict__ k, int64_t N, int32_t *__restrict__ f) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    f[p] = (p > 0 && k[p] != k[p - 1]) ? 1 : 0;
+}
+
+__global__ void k_scatter_rank(const int32_t *__restrict__ who, const int32_t *__restrict__ dense,
+                               int64_t N, int MP, int col, uint32_t *__restrict__ R) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    R[(int64_t)who[p] * MP + col] = (uint32_t)dense[p];
+}
+
+__global__ void k_iota(int32_t *v, int64_t N) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p < N) v[p] = (int32_t)p;
+}
+
+// pack columns [c0, c0+g) of the rank tuple of row perm[p] into one u64 key
+__global__ void k_pack_keys(const uint32_t *__restrict__ R, const int32_t *__restrict__ perm,
+                            int64_t N, int MP, int c0, int g, int bits, uint64_t *__restrict__ keys) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const uint32_t *r = R + (int64_t)perm[p] * MP;
+    uint64_t k = 0;
+    for (int c = c0; c < c0 + g; ++c) k = (k << bits) | r[c];
+    keys[p] = k;
+}
+
+// v[p] = p at the start of each run of equal tuples (0 otherwise); max-scan -> run id
+__global__ void k_tuple_start(const uint32_t *__restrict__ R, const int32_t *__restrict__ order,
+                              int64_t N, int m, int MP, int32_t *__restrict__ v) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    int start = 1;
+    if (p > 0) {
+        const uint32_t *a = R + (int64_t)order[p] * MP;
+        const uint32_t *b = R + (int64_t)order[p - 1] * MP;
+        start = 0;
+        for (int c = 0; c < m; ++c) start |= (a[c] != b[c]);
+    }
+    v[p] = start ? (int32_t)p : 0;
+}
+
+// record p (lex order): {r1, ..., r_{m-1}, id, 0 ...}; padding rows all-ones
+__global__ void k_records(const uint32_t *__restrict__ R, const int32_t *__restrict__ order,
+                          const int32_t *__restrict__ id, int64_t N, int64_t Np, int m, int MP,
+                          int NV, uint4 *__restrict__ rec) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= Np) return;
+    uint32_t f[16];
+    if (p < N) {
+        const uint32_t *r = R + (int64_t)order[p] * MP;
+        for (int c = 0; c < 4 * NV; ++c) f[c] = c + 1 < m ? r[c + 1] : 0u;
+        f[m - 1] = (uint32_t)id[p];
+    } else {
+        for (int c = 0; c < 4 * NV; ++c) f[c] = 0xFFFFFFFFu;
+    }
+    for (int v = 0; v < NV; ++v)
+        rec[p * NV + v] = make_uint4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
+}
+
+__global__ void k_rowtile_offsets(int64_t nT, int64_t W, int64_t *off) {
+    int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (I >= nT) return;
+    off[I] = (int64_t)TILE * (I * W - 8 * I * (I - 1) / 2);
+}
+
+// ------------------------------------------------------------------ K1
+__device__ __forceinline__ uint32_t fld(const uint4 *r, int k) {
+    const uint4 v = r[k >> 2];
+    switch (k & 3) {
+        case 0: return v.x;
+        case 1: return v.y;
+        case 2: return v.z;
+        default: return v.w;
+    }
+}
+
+// items before strip T when strip t owns floor(t/CHUNK)+1 items
+__device__ __forceinline__ int64_t items_before(int64_t T) {
+    int64_t a = T / CHUNK, r = T % CHUNK;
+    return T + CHUNK * a * (a - 1) / 2 + r * a;
+}
+
+template <int M>
+__global__ void __launch_bounds__(TILE) k_dom_bits(const uint4 *__restrict__ rec, int64_t N,
+                                                   int64_t nT, int64_t W,
+                                                   const int64_t *__restrict__ rt_off,
+                                                   uint32_t *__restrict__ bits) {
+    constexpr int NV = (M + 3) / 4;
+    __shared__ uint4 sI[TILE * NV];
+    __shared__ __align__(16) uint32_t sB[TILE * 8];
+    __shared__ int64_t s_jt, s_chunk;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        int64_t item = blockIdx.x, lo = 0, hi = nT - 1;
+        while (lo < hi) {
+            int64_t mid = (lo + hi + 1) >> 1;
+            if (items_before(mid) <= item) lo = mid; else hi = mid - 1;
+        }
+        s_jt = lo;
+        s_chunk = item - items_before(lo);
+    }
+    __syncthreads();
+    const int64_t jt = s_jt, chunk = s_chunk;
+    const int64_t j = jt * TILE + tid;
+    uint4 rj[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) rj[v] = rec[j * NV + v];
+    const uint32_t jmin_id = fld(&rec[jt * TILE * NV], M - 1);
+    const int64_t it0 = chunk * CHUNK;
+    const int64_t it1 = min(it0 + CHUNK, jt + 1);
+    for (int64_t it = it0; it < it1; ++it) {
+        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sI[tid * NV + v] = rec[(it * TILE + tid) * NV + v];
+        __syncthreads();
+        const bool disjoint = fld(&sI[(TILE - 1) * NV], M - 1) < jmin_id;
+        if (disjoint) {
+#pragma unroll 8
+            for (int i = 0; i < TILE; ++i) {
+                bool P = true;
+#pragma unroll
+                for (int k = 0; k < M - 1; ++k) P &= fld(&sI[i * NV], k) <= fld(rj, k);
+                const uint32_t b = __ballot_sync(~0u, P);
+                if (lane == 0) sB[i * 8 + warp] = b;
+            }
+        } else {
+#pragma unroll 4
+            for (int i = 0; i < TILE; ++i) {
+                bool P = fld(&sI[i * NV], M - 1) < fld(rj, M - 1);
+#pragma unroll
+                for (int k = 0; k < M - 1; ++k) P &= fld(&sI[i * NV], k) <= fld(rj, k);
+                const uint32_t b = __ballot_sync(~0u, P);
+                if (lane == 0) sB[i * 8 + warp] = b;
+            }
+        }
+        __syncthreads();
+        const int64_t i = it * TILE + tid;
+        if (i < N) {
+            uint32_t *dst = bits + rt_off[it] + (int64_t)tid * (W - 8 * it) + 8 * (jt - it);
+            const uint4 *src = reinterpret_cast<const uint4 *>(sB) + tid * 2;
+            uint4 lo = src[0], hi = src[1];
+            if (jt == nT - 1) {  // columns past N carry padding records: mask them
+                uint32_t w8[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int64_t base = jt * TILE + 32 * q;
+                    const uint32_t vm = base + 32 <= N ? ~0u : (base >= N ? 0u : (1u << (N - base)) - 1u);
+                    w8[q] &= vm;
+                }
+                lo = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+                hi = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+            }
+            reinterpret_cast<uint4 *>(dst)[0] = lo;
+            reinterpret_cast<uint4 *>(dst)[1] = hi;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K2
+struct PeelArgs {
+    const uint32_t *bits;
+    const int64_t *rt_off;
+    int64_t W;
+    int N, NB, n, mode;
+    int32_t *cnt, *rank_s, *list, *blkcnt;
+    int32_t *out_l, *out_nfronts, *status;
+};
+
+// in-place exclusive scan of s[0..len) (len <= 4096) by one CTA of PEEL_T threads;
+// returns the total.  Uses `tmp` (PEEL_T/32 ints).
+__device__ int block_exclusive_scan(int *s, int len, int *tmp) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (len + PEEL_T - 1) / PEEL_T;
+    const int lo = tid * per, hi = min(lo + per, len);
+    int sum = 0;
+    for (int q = lo; q < hi; ++q) sum += s[q];
+    int incl = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int y = __shfl_up_sync(~0u, incl, d);
+        if (lane >= d) incl += y;
+    }
+    if (lane == 31) tmp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int v = lane < PEEL_T / 32 ? tmp[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int y = __shfl_up_sync(~0u, v, d);
+            if (lane >= d) v += y;
+        }
+        if (lane < PEEL_T / 32) tmp[lane] = v;
+    }
+    __syncthreads();
+    int run = incl - sum + (warp ? tmp[warp - 1] : 0);
+    const int total = tmp[PEEL_T / 32 - 1];
+    for (int q = lo; q < hi; ++q) {
+        int v = s[q];
+        s[q] = run;
+        run += v;
+    }
+    __syncthreads();
+    return total;
+}
+
+// Subtract (sign=-1) or add (sign=+1) the bits of listed rows into cnt.
+// rows_below[wb] (wb < NB) = number of list rows with index < 1024*(wb+1);
+// item_pref = exclusive prefix of ceil(rows_below/LC).
+__device__ void vertical_pass(const PeelArgs &a, const int *rows_below, const int *item_pref,
+                              bool identity, int sign, uint32_t *sred) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int total = item_pref[a.NB];
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        int lo = 0, hi = a.NB - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (item_pref[mid] <= item) lo = mid; else hi = mid - 1;
+        }
+        const int wb = lo;
+        const int chunk = item - item_pref[wb];
+        const int r0 = chunk * LC + warp * ROWS_PER_WARP;
+        const int r1 = min(r0 + ROWS_PER_WARP, rows_below[wb]);
+        const int64_t w = (int64_t)wb * 32 + lane;
+        uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0, o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+        for (int g = r0; g < r1; g += 15) {
+            const int ge = min(g + 15, r1);
+            uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll 5
+            for (int r = g; r < ge; ++r) {
+                const int i = identity ? r : a.list[r];
+                const int64_t it = i >> 8;
+                uint32_t x = 0;
+                if (w >= 8 * it)
+                    x = __ldg(a.bits + a.rt_off[it] + (int64_t)(i & 255) * (a.W - 8 * it) + (w - 8 * it));
+                a0 += x & 0x11111111u;
+                a1 += (x >> 1) & 0x11111111u;
+                a2 += (x >> 2) & 0x11111111u;
+                a3 += (x >> 3) & 0x11111111u;
+            }
+            e0 += a0 & 0x0F0F0F0Fu; o0 += (a0 >> 4) & 0x0F0F0F0Fu;
+            e1 += a1 & 0x0F0F0F0Fu; o1 += (a1 >> 4) & 0x0F0F0F0Fu;
+            e2 += a2 & 0x0F0F0F0Fu; o2 += (a2 >> 4) & 0x0F0F0F0Fu;
+            e3 += a3 & 0x0F0F0F0Fu; o3 += (a3 >> 4) & 0x0F0F0F0Fu;
+        }
+        uint32_t *mine = sred + warp * 8 * 32 + lane;
+        mine[0 * 32] = e0; mine[1 * 32] = e1; mine[2 * 32] = e2; mine[3 * 32] = e3;
+        mine[4 * 32] = o0; mine[5 * 32] = o1; mine[6 * 32] = o2; mine[7 * 32] = o3;
+        __syncthreads();
+        {
+            const int q = tid >> 5, l = tid & 31;  // q: which byte register, l: word column
+            uint32_t s = 0;
+#pragma unroll
+            for (int ww = 0; ww < 8; ++ww) s += sred[(ww * 8 + q) * 32 + l];
+            const int64_t col = ((int64_t)wb * 32 + l) * 32;
+            const int kk = q & 3, half = q >> 2;
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) {
+                const int c = (s >> (8 * nb)) & 255;
+                if (c) atomicAdd(a.cnt + col + 8 * nb + 4 * half + kk, sign * c);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(PEEL_T) k_peel(PeelArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ int psm[];
+    int *s_rows = psm;                 // NB + 1
+    int *s_items = psm + (a.NB + 1);   // NB + 1
+    int *s_tmp = s_items + (a.NB + 1); // 32
+    uint32_t *sred = reinterpret_cast<uint32_t *>(s_tmp + 32);  // 8*8*32
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // ---- initial dominated-by counts: all rows, identity list, sign +1
+    for (int wb = tid; wb < a.NB; wb += PEEL_T) {
+        const int rb = min(a.N, (wb + 1) * 1024);
+        s_rows[wb] = rb;
+        s_items[wb] = (rb + LC - 1) / LC;
+    }
+    if (tid == 0) s_items[a.NB] = 0;
+    __syncthreads();
+    block_exclusive_scan(s_items, a.NB + 1, s_tmp);
+    vertical_pass(a, s_rows, s_items, true, +1, sred);
+    grid.sync();
+
+    int ranked = 0, l = -1, k = 0;
+    while (true) {
+        // A1: front rows per 1024-row block
+        for (int wb = blockIdx.x; wb < a.NB; wb += gridDim.x) {
+            int c = 0;
+            for (int t = tid; t < 1024; t += PEEL_T) {
+                const int i = wb * 1024 + t;
+                c += (i < a.N && a.rank_s[i] < 0 && a.cnt[i] == 0);
+            }
+            c = __reduce_add_sync(~0u, c);
+            if (lane == 0) s_tmp[warp] = c;
+            __syncthreads();
+            if (tid == 0) {
+                int s = 0;
+                for (int q = 0; q < PEEL_T / 32; ++q) s += s_tmp[q];
+                a.blkcnt[wb] = s;
+            }
+            __syncthreads();
+        }
+        grid.sync();
+        // A2: ordered compaction of the front, ranks := k
+        for (int wb = tid; wb <= a.NB; wb += PEEL_T) s_rows[wb] = wb < a.NB ? a.blkcnt[wb] : 0;
+        __syncthreads();
+        const int total = block_exclusive_scan(s_rows, a.NB + 1, s_tmp);  // s_rows[wb] = start
+        if (total == 0) {
+            if (ranked < a.N && blockIdx.x == 0 && tid == 0) flag_status(a.status, TEMO_ST_PEEL);
+            break;
+        }
+        for (int wb = blockIdx.x; wb < a.NB; wb += gridDim.x) {
+            int base = s_rows[wb];
+            for (int t0 = 0; t0 < 1024; t0 += PEEL_T) {
+                const int i = wb * 1024 + t0 + tid;
+                const bool f = i < a.N && a.rank_s[i] < 0 && a.cnt[i] == 0;
+                const uint32_t bal = __ballot_sync(~0u, f);
+                if (lane == 0) s_tmp[warp] = __popc(bal);
+                __syncthreads();
+                int before = 0, chunk_total = 0;
+                for (int q = 0; q < PEEL_T / 32; ++q) {
+                    before += q < warp ? s_tmp[q] : 0;
+                    chunk_total += s_tmp[q];
+                }
+                if (f) {
+                    a.list[base + before + __popc(bal & ((1u << lane) - 1))] = i;
+                    a.rank_s[i] = k;
+                }
+                base += chunk_total;
+                __syncthreads();
+            }
+        }
+        ranked += total;
+        if (l < 0 && ranked >= a.n) l = k;
+        ++k;
+        if ((a.mode == TEMO_RANK_SELECT && ranked >= a.n) || ranked >= a.N || k > a.N) break;
+        grid.sync();
+        // B: subtract the front's bits.  s_rows holds exclusive starts with
+        // s_rows[NB] = total, so rows_below(wb) = s_rows[wb + 1].
+        for (int wb = tid; wb <= a.NB; wb += PEEL_T)
+            s_items[wb] = wb < a.NB ? (s_rows[wb + 1] + LC - 1) / LC : 0;
+        __syncthreads();
+        block_exclusive_scan(s_items, a.NB + 1, s_tmp);
+        vertical_pass(a, s_rows + 1, s_items, false, -1, sred);
+        grid.sync();
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        *a.out_l = l;
+        if (a.out_nfronts) *a.out_nfronts = k;
+    }
+}
+
+__global__ void k_peel_init(int32_t *rank_s, int32_t *cnt, int64_t N, int64_t Np) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= Np) return;
+    rank_s[p] = p < N ? -1 : 0x7FFFFFFF;
+    cnt[p] = 0;
+}
+
+__global__ void k_unsort_ranks(const int32_t *__restrict__ rank_s, const int32_t *__restrict__ order,
+                               const int32_t *__restrict__ l, int64_t N, int32_t *__restrict__ rank) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const int32_t r = rank_s[p];
+    rank[order[p]] = r < 0 ? *l + 1 : r;
+}
+
+// expand the packed bitmap to the dense N x ceil(N/32) layout of original indices
+__global__ void k_expand_dense(const uint32_t *__restrict__ bits, const int64_t *__restrict__ rt_off,
+                               int64_t W, const int32_t *__restrict__ pos, int64_t N, int64_t Wd,
+                               uint32_t *__restrict__ D) {
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= N * Wd) return;
+    const int64_t i = q / Wd, jw = q % Wd;
+    const int64_t pi = pos[i], it = pi >> 8;
+    uint32_t word = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int64_t j = jw * 32 + b;
+        if (j >= N) break;
+        const int64_t pj = pos[j];
+        if (pj <= pi) continue;
+        const int64_t w = pj >> 5;
+        const uint32_t x = bits[rt_off[it] + (pi & 255) * (W - 8 * it) + (w - 8 * it)];
+        word |= ((x >> (pj & 31)) & 1u) << b;
+    }
+    D[q] = word;
+}
+
+__global__ void k_inverse(const int32_t *__restrict__ order, int64_t N, int32_t *__restrict__ pos) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p < N) pos[order[p]] = (int32_t)p;
+}
+
+// ------------------------------------------------------------------ host
+static inline dim3 grid1(int64_t n, int t = 256) { return dim3((unsigned)((n + t - 1) / t)); }
+
+// K0 + records + K1.  Leaves order in p.vals_a, records in p.rec, bitmap in p.bits.
+static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStream_t st) {
+    const int64_t N = p.N;
+    const int m = p.m, MP = 4 * p.NV;
+    size_t tb = p.cub_bytes;
+    // K0: per-column dense ranks
+    for (int col = 0; col < m; ++col) {
+        k_col_keys<<<grid1(N), 256, 0, st>>>(F, N, m, col, p.keys_a, p.vals_a, status);
+        TEMO_CUDA(cub::DeviceRadixSort::SortPairs(p.cub_tmp, tb, p.keys_a, p.keys_b, p.vals_a,
+                                                  p.vals_b, (int)N, 0, 64, st));
+        k_key_change<<<grid1(N), 256, 0, st>>>(p.keys_b, N, p.scan_a);
+        TEMO_CUDA(cub::DeviceScan::InclusiveSum(p.cub_tmp, tb, p.scan_a, p.scan_b, (int)N, st));
+        k_scatter_rank<<<grid1(N), 256, 0, st>>>(p.vals_b, p.scan_b, N, MP, col, p.R);
+    }
+    // lexicographic order of rank tuples: LSD passes, several columns per u64 key
+    k_iota<<<grid1(N), 256, 0, st>>>(p.vals_a, N);
+    const int per = 64 / p.bitsN;
+    for (int hi = m; hi > 0;) {
+        const int g = hi < per ? hi : per;
+        const int c0 = hi - g;
+        k_pack_keys<<<grid1(N), 256, 0, st>>>(p.R, p.vals_a, N, MP, c0, g, p.bitsN, p.keys_a);
+        TEMO_CUDA(cub::DeviceRadixSort::SortPairs(p.cub_tmp, tb, p.keys_a, p.keys_b, p.vals_a,
+                                                  p.vals_b, (int)N, 0, g * p.bitsN, st));
+        std::swap(p.vals_a, p.vals_b);
+        hi = c0;
+    }
+    // run ids of equal tuples
+    k_tuple_start<<<grid1(N), 256, 0, st>>>(p.R, p.vals_a, N, m, MP, p.scan_a);
+    TEMO_CUDA(cub::DeviceScan::InclusiveScan(p.cub_tmp, tb, p.scan_a, p.scan_b, cub::Max(), (int)N, st));
+    k_records<<<grid1(p.Np), 256, 0, st>>>(p.R, p.vals_a, p.scan_b, N, p.Np, m, MP, p.NV, p.rec);
+    k_rowtile_offsets<<<grid1(p.nT), 256, 0, st>>>(p.nT, p.W, p.rt_off);
+    TEMO_LAUNCH_CHECK();
+    // K1
+    const int64_t items = p.nT + CHUNK * ((p.nT / CHUNK) * ((p.nT / CHUNK) - 1) / 2) +
+                          (p.nT % CHUNK) * (p.nT / CHUNK);
+    const dim3 g((unsigned)items);
+#define DOM_CASE(MM) \
+    case MM: k_dom_bits<MM><<<g, TILE, 0, st>>>(p.rec, N, p.nT, p.W, p.rt_off, p.bits); break;
+    switch (m) {
+        DOM_CASE(1) DOM_CASE(2) DOM_CASE(3) DOM_CASE(4) DOM_CASE(5) DOM_CASE(6) DOM_CASE(7)
+        DOM_CASE(8) DOM_CASE(9) DOM_CASE(10) DOM_CASE(11) DOM_CASE(12) DOM_CASE(13) DOM_CASE(14)
+        DOM_CASE(15) DOM_CASE(16)
+        default: return TEMO_EINVAL;
+    }
+#undef DOM_CASE
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
+static int peel_grid(int NB, size_t smem) {
+    static int occ = 0;
+    if (!occ) {
+        cudaFuncSetAttribute(k_peel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_peel, PEEL_T, 24 * 1024);
+        if (occ <= 0) occ = 1;
+    }
+    (void)smem;
+    int P = num_sms() * occ;
+    const int want = NB * 16;
+    return want < P ? (want > 0 ? want : 1) : P;
+}
+
+}  // namespace temo
+
+using namespace temo;
+
+extern "C" size_t temo_rank_ws_bytes(int64_t N, int m) {
+    if (N < 1 || m < 1 || m > MAX_M) return 0;
+    RankPlan p;
+    plan_rank(p, nullptr, N, m);
+    return p.total;
+}
+
+extern "C" int temo_rank(const double *F, int64_t N, int m, int64_t n, int mode, int32_t *rank,
+                         int32_t *l_out, int32_t *nfronts, int32_t *status, void *ws,
+                         size_t ws_bytes, temo_stream_t stream) {
+    if (N < 1 || N > (1 << 20) || m < 1 || m > MAX_M) return TEMO_EINVAL;
+    if (n < 1 || n > N) return TEMO_EINVAL;
+    if (mode != TEMO_RANK_SORT && mode != TEMO_RANK_SELECT) return TEMO_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    RankPlan p;
+    plan_rank(p, nullptr, N, m);
+    if (ws_bytes < p.total || !ws) return TEMO_EWORKSPACE;
+    plan_rank(p, ws, N, m);
+    int rc = build_bitmap(p, F, status, st);
+    if (rc) return rc;
+    k_peel_init<<<grid1(p.Np), 256, 0, st>>>(p.rank_s, p.cnt, N, p.Np);
+    PeelArgs a;
+    a.bits = p.bits;
+    a.rt_off = p.rt_off;
+    a.W = p.W;
+    a.N = (int)N;
+    a.NB = (int)p.NB;
+    a.n = (int)n;
+    a.mode = mode;
+    a.cnt = p.cnt;
+    a.rank_s = p.rank_s;
+    a.list = p.list;
+    a.blkcnt = p.blkcnt;
+    a.out_l = l_out;
+    a.out_nfronts = nfronts;
+    a.status = status;
+    const size_t smem = (size_t)(2 * (p.NB + 1) + 32) * sizeof(int) + 8 * 8 * 32 * sizeof(uint32_t);
+    const int P = peel_grid((int)p.NB, smem);
+    void *args[] = {&a};
+    TEMO_CUDA(cudaLaunchCooperativeKernel((void *)k_peel, dim3(P), dim3(PEEL_T), args, smem, st));
+    k_unsort_ranks<<<grid1(N), 256, 0, st>>>(p.rank_s, p.vals_a, l_out, N, rank);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
+extern "C" size_t temo_dominance_ws_bytes(int64_t N, int m) {
+    return temo_rank_ws_bytes(N, m) + (size_t)N * 4 + 256;
+}
+
+extern "C" int temo_dominance(const double *F, int64_t N, int m, uint32_t *D_out, int32_t *status,
+                              void *ws, size_t ws_bytes, temo_stream_t stream) {
+    if (N < 1 || N > (1 << 20) || m < 1 || m > MAX_M) return TEMO_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    RankPlan p;
+    plan_rank(p, nullptr, N, m);
+    if (ws_bytes < p.total + (size_t)N * 4 + 256 || !ws) return TEMO_EWORKSPACE;
+    plan_rank(p, ws, N, m);
+    int32_t *pos = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + round_up(p.total, 256));
+    int rc = build_bitmap(p, F, status, st);
+    if (rc) return rc;
+    k_inverse<<<grid1(N), 256, 0, st>>>(p.vals_a, N, pos);
+    const int64_t Wd = (N + 31) / 32;
+    k_expand_dense<<<grid1(N * Wd), 256, 0, st>>>(p.bits, p.rt_off, p.W, pos, N, Wd, D_out);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}

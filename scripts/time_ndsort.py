@@ -1,0 +1,35 @@
+"""Time the GPU ND sort at several sizes (CUDA events on the launching stream)."""
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2503_20286_b200.ndsort import SELECT, SORT, rank_device  # noqa: E402
+
+
+def main():
+    sizes = [int(a) for a in sys.argv[1:]] or [20000, 100000, 400000]
+    for m in (3,):
+        for N in sizes:
+            F = torch.from_numpy(np.random.default_rng(0).random((N, m))).cuda()
+            for mode in (SORT, SELECT):
+                rank_device(F, N // 2, mode)
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                reps = 3
+                for _ in range(reps):
+                    r, l, nf = rank_device(F, N // 2, mode)
+                e.record()
+                torch.cuda.synchronize()
+                ms = s.elapsed_time(e) / reps
+                print(json.dumps(dict(N=N, m=m, mode=mode, ms=round(ms, 3), fronts=int(nf.item()),
+                                      l=int(l.item()), pairs_per_s=N * (N - 1) / ms * 1e3)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+"""GPU parity: ND sort (K0-K2) against golden reference vectors and the CPU oracle."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, unpack
+from oracle import ndsort as ond
+
+pytestmark = pytest.mark.gpu
+
+
+def test_rank_golden_all(cuda):
+    from paper_2503_20286_b200 import rank_assign
+
+    z = load_golden("ndsort")
+    for i in range(len(z["N"])):
+        N, m, n = int(z["N"][i]), int(z["m"][i]), int(z["n"][i])
+        F = unpack(z["F"], z["F_off"], i).reshape(N, m)
+        res = rank_assign(F, n)
+        assert np.array_equal(res.r, unpack(z["r"], z["r_off"], i)), i
+        assert res.l == int(z["l"][i]), i
+
+
+def test_dominance_matrix_golden_small(cuda):
+    from paper_2503_20286_b200 import dominance_matrix
+
+    z = load_golden("ndsort")
+    for i in range(0, 500, 7):
+        N, m = int(z["N"][i]), int(z["m"][i])
+        F = unpack(z["F"], z["F_off"], i).reshape(N, m)
+        assert np.array_equal(dominance_matrix(F), ond.dominance_matrix(F)), i
+
+
+# -- ports of the reference's own tests (test_ndsort.py) ---------------------
+def test_known_answers(cuda):
+    from paper_2503_20286_b200 import dominance_matrix, rank_assign
+
+    assert dominance_matrix(np.array([[1.0, 1.0], [1.0, 1.0]])).sum() == 0
+    D = dominance_matrix(np.array([[0.0, 0.0], [1.0, 2.0], [2.0, 1.0]]))
+    assert D.tolist() == [[0, 1, 1], [0, 0, 0], [0, 0, 0]]
+    res = rank_assign(np.array([[0.0, 0.0], [1.0, 1.0], [2.0, 2.0]]), 2)
+    assert res.r.tolist() == [0, 1, 2] and res.l == 1
+    res = rank_assign(np.array([[0.0, 0.0], [1.0, 2.0], [2.0, 1.0]]), 2)
+    assert res.r.tolist() == [0, 1, 1] and res.l == 1
+    r = rank_assign(np.array([[1.0, 2.0], [1.0, 2.0], [0.5, 3.0]]), 2).r
+    assert r.tolist() == [0, 0, 0]
+    assert rank_assign(np.array([[0.0, 1.0], [1.0, 0.0]]), 2).l == 0
+
+
+def test_errors(cuda):
+    from paper_2503_20286_b200 import dominance_matrix, rank_assign
+
+    with pytest.raises(ValueError):
+        dominance_matrix(np.array([[0.0, np.nan]]))
+    with pytest.raises(ValueError):
+        rank_assign(np.array([[0.0, np.nan], [1.0, 1.0]]), 1)
+    with pytest.raises(ValueError):
+        rank_assign(np.zeros((3, 2)), 4)
+    with pytest.raises(ValueError):
+        rank_assign(np.zeros((3, 2)), 0)
+
+
+def test_nan_on_device_tensor_flags_status(cuda):
+    import torch
+
+    from paper_2503_20286_b200 import rank_assign
+
+    F = torch.rand(100, 3, dtype=torch.float64, device=cuda)
+    F[17, 1] = float("nan")
+    with pytest.raises(ValueError):
+        rank_assign(F, 10)
+
+
+def test_permutation_equivariance_and_contiguity(cuda):
+    from paper_2503_20286_b200 import rank_assign
+
+    rng = np.random.default_rng(65)
+    F = rng.integers(0, 4, size=(25, 3)).astype(float)
+    base = rank_assign(F, 10).r
+    for _ in range(10):
+        perm = rng.permutation(25)
+        assert np.array_equal(rank_assign(F[perm], 10).r, base[perm])
+    for _ in range(20):
+        r = rank_assign(rng.random((300, 3)), 10).r
+        assert set(r.tolist()) == set(range(int(r.max()) + 1))
+
+
+@pytest.mark.parametrize("N,m,kind", [(3000, 3, "u"), (5000, 2, "u"), (4097, 5, "i"), (2000, 10, "u"),
+                                      (1025, 16, "u"), (6000, 3, "dtlz2"), (257, 1, "i")])
+def test_rank_vs_oracle_mid(cuda, N, m, kind):
+    from paper_2503_20286_b200 import rank_assign
+
+    rng = np.random.default_rng(N + m)
+    if kind == "u":
+        F = rng.random((N, m))
+    elif kind == "i":
+        F = rng.integers(0, 7, size=(N, m)).astype(float)
+    else:
+        from oracle.problems import evaluate_dtlz
+
+        F = evaluate_dtlz("dtlz2", rng.random((N, m + 9)), m)
+    n = N // 2
+    got = rank_assign(F, n)
+    want_r, want_l = ond.rank_fast(F, n)
+    assert np.array_equal(got.r, want_r) and got.l == want_l
+
+
+def test_select_mode_matches_sort_below_l(cuda):
+    import torch
+
+    from paper_2503_20286_b200.ndsort import SELECT, SORT, rank_device
+
+    rng = np.random.default_rng(5)
+    F = torch.from_numpy(rng.random((50000, 3))).cuda()
+    n = 25000
+    r_sort, l_sort, nf_sort = rank_device(F, n, SORT)
+    r_sel, l_sel, nf_sel = rank_device(F, n, SELECT)
+    l = int(l_sort.item())
+    assert l == int(l_sel.item())
+    rs, rl = r_sort.cpu().numpy(), r_sel.cpu().numpy()
+    keep = rs <= l
+    assert np.array_equal(rs[keep], rl[keep])
+    assert np.all(rl[~keep] == l + 1)
+    assert int(nf_sel.item()) == l + 1 <= int(nf_sort.item())
+
+
+def test_large_property_equivariance(cuda):
+    """N=200k (beyond the reference's memory limit): ranks are permutation-equivariant,
+    contiguous, and rank 0 == rows not dominated by any rank-0 row (size-independent checks)."""
+    import torch
+
+    from paper_2503_20286_b200.ndsort import SORT, rank_device
+
+    rng = np.random.default_rng(11)
+    N = 200_000
+    F = rng.random((N, 3))
+    perm = rng.permutation(N)
+    r1 = rank_device(torch.from_numpy(F).cuda(), N // 2, SORT)[0].cpu().numpy()
+    r2 = rank_device(torch.from_numpy(F[perm]).cuda(), N // 2, SORT)[0].cpu().numpy()
+    assert np.array_equal(r2, r1[perm])
+    assert set(np.unique(r1).tolist()) == set(range(int(r1.max()) + 1))
+    # spot-check 300 random rows against the definition of rank
+    for j in rng.choice(N, 300, replace=False):
+        dom = np.all(F <= F[j], axis=1) & np.any(F < F[j], axis=1)
+        want = 0 if not dom.any() else int(r1[dom].max()) + 1
+        assert r1[j] == want
