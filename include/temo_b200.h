@@ -75,6 +75,66 @@ size_t temo_dominance_ws_bytes(int64_t N, int m);
 int temo_dominance(const double *F, int64_t N, int m, uint32_t *D_out, int32_t *status,
                    void *ws, size_t ws_bytes, temo_stream_t stream);
 
+/* ---------------------------------------------------------- NSGA-III select
+ * Replaces nsga3.py:207-218 (normalize, associate, niche_counts, niche_select,
+ * update_rank, keep) on already-shuffled objectives Fs (N x m) whose ranks
+ * come from temo_rank(..., TEMO_RANK_SELECT) (`rank` is updated in place to
+ * the final ranks; `l` is the device scalar from temo_rank).
+ *   W (nr x m) directions; keep (n int32) receives flatnonzero(rank < l).
+ *   pi, dist (N) association (nsga3.py:96-116; excluded rows pi=0, dist=NaN);
+ *   icpt (m), promoted (<= nr, direction order) always written;
+ *   Fp (N x m), ideal (m), extreme (m int64), rho/rho_l (nr), counts (8 int32:
+ *   n_promoted, n_s, n_dif, -, kept) optional (NULL to skip). */
+size_t temo_nsga3_select_ws_bytes(int64_t N, int m, int64_t nr);
+int temo_nsga3_select(const double *Fs, int64_t N, int m, const double *W, int64_t nr, int64_t n,
+                      int32_t *rank, const int32_t *l, int32_t *keep, int32_t *pi, double *dist,
+                      double *Fp, double *ideal, double *icpt, int64_t *extreme, int32_t *rho,
+                      int32_t *rho_l, int32_t *promoted, int32_t *counts, int32_t *status, void *ws,
+                      size_t ws_bytes, temo_stream_t stream);
+
+/* Standalone stages (same kernels as temo_nsga3_select), one per reference function:
+ *   temo_nsga3_normalize  nsga3.normalize   (nsga3.py:61-93)  rows with NaN are excluded
+ *   temo_associate        nsga3.associate   (nsga3.py:96-116)
+ *   temo_niche_counts     nsga3.niche_counts (nsga3.py:119-123)
+ *   temo_niche_select     nsga3.niche_select (nsga3.py:126-167), counts[0] = #promoted
+ *   temo_update_rank      nsga3.update_rank  (nsga3.py:170-183)
+ * All share the workspace size temo_nsga3_select_ws_bytes(N, m, nr). */
+int temo_nsga3_normalize(const double *F, int64_t N, int m, double *Fp, double *ideal, double *icpt,
+                         int64_t *extreme, void *ws, size_t ws_bytes, temo_stream_t stream);
+int temo_associate(const double *Fp, int64_t N, int m, const double *W, int64_t nr, int32_t *pi,
+                   double *dist, void *ws, size_t ws_bytes, temo_stream_t stream);
+int temo_niche_counts(const int32_t *rank, const int32_t *pi, int64_t N, int32_t l, int64_t nr,
+                      int32_t *rho, int32_t *rho_l, void *ws, size_t ws_bytes, temo_stream_t stream);
+int temo_niche_select(int32_t *rank, const int32_t *pi, const double *dist, int64_t N, int32_t l,
+                      const int32_t *rho, int64_t nr, int32_t *promoted, int32_t *counts, void *ws,
+                      size_t ws_bytes, temo_stream_t stream);
+int temo_update_rank(int32_t *rank, int64_t N, const int32_t *promoted, int64_t n_promoted,
+                     int64_t n_dif, int32_t l, int32_t *status, void *ws, size_t ws_bytes,
+                     temo_stream_t stream);
+
+/* Row gathers used to materialise survivors (X[perm][keep]):
+ *   dst[r] = src[idx[r]]            (idx32 or idx64, the other NULL)
+ *   dst[r] = src[idx_a[idx_b[r]]]   (composed permutation) */
+int temo_gather_rows(const double *src, const int32_t *idx32, const int64_t *idx64, int64_t rows,
+                     int64_t cols, double *dst, temo_stream_t stream);
+int temo_gather_rows2(const double *src, const int64_t *idx_a, const int32_t *idx_b, int64_t rows,
+                      int64_t cols, double *dst, temo_stream_t stream);
+
+/* --------------------------------------------------------------- directions
+ * directions.neighbors (directions.py:104-114): out (r x T int32) holds the T
+ * nearest rows of W (r x m) by Euclidean distance, ties to the lower index.
+ * 1 <= T <= min(r, 64), m <= 16. */
+int temo_neighbors(const double *W, int64_t r, int m, int T, int32_t *out, temo_stream_t stream);
+
+/* ------------------------------------------------------------ stage timing
+ * CUDA-event timing of each kernel stage on its own stream (off by default).
+ * temo_timing_read syncs the recorded events, fills ms_out/calls_out
+ * (TEMO_STAGE_COUNT entries each) and optionally resets the accumulators. */
+#define TEMO_STAGE_COUNT 14
+void temo_timing_enable(int on);
+const char *temo_timing_name(int stage);
+int temo_timing_read(double *ms_out, int64_t *calls_out, int reset);
+
 #ifdef __cplusplus
 }
 #endif

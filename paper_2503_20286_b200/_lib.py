@@ -30,7 +30,22 @@ SIGNATURES = {
     "temo_rank": (_I32, [_P, _I64, _I32, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "temo_dominance_ws_bytes": (_SZ, [_I64, _I32]),
     "temo_dominance": (_I32, [_P, _I64, _I32, _P, _P, _P, _SZ, _P]),
+    "temo_nsga3_select_ws_bytes": (_SZ, [_I64, _I32, _I64]),
+    "temo_nsga3_select": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P,
+                                 _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "temo_nsga3_normalize": (_I32, [_P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
+    "temo_associate": (_I32, [_P, _I64, _I32, _P, _I64, _P, _P, _P, _SZ, _P]),
+    "temo_niche_counts": (_I32, [_P, _P, _I64, _I32, _I64, _P, _P, _P, _SZ, _P]),
+    "temo_niche_select": (_I32, [_P, _P, _P, _I64, _I32, _P, _I64, _P, _P, _P, _SZ, _P]),
+    "temo_update_rank": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _SZ, _P]),
+    "temo_gather_rows": (_I32, [_P, _P, _P, _I64, _I64, _P, _P]),
+    "temo_gather_rows2": (_I32, [_P, _P, _P, _I64, _I64, _P, _P]),
+    "temo_neighbors": (_I32, [_P, _I64, _I32, _I32, _P, _P]),
+    "temo_timing_enable": (None, [_I32]),
+    "temo_timing_name": (ctypes.c_char_p, [_I32]),
+    "temo_timing_read": (_I32, [_P, _P, _I32]),
 }
+STAGE_COUNT = 14
 
 TEMO_OK, TEMO_EINVAL, TEMO_ENAN, TEMO_ERUNTIME, TEMO_EWORKSPACE, TEMO_ECUDA = range(6)
 ST_NAN, ST_PEEL, ST_FILL, ST_DEMOTE, ST_COUNT, ST_KRANGE = 1, 2, 4, 8, 16, 32
@@ -172,3 +187,36 @@ def new_status(dev):
 def sync_status(status, what):
     bits = int(status.item())
     raise_status(bits, what)
+
+
+def timing_enable(on: bool = True):
+    lib().temo_timing_enable(1 if on else 0)
+
+
+def timing_read(reset: bool = True) -> dict:
+    """{stage name: (ms, calls)} accumulated since the last reset (syncs the events)."""
+    ms = np.zeros(STAGE_COUNT, dtype=np.float64)
+    calls = np.zeros(STAGE_COUNT, dtype=np.int64)
+    L = lib()
+    L.temo_timing_read(_P(ms.ctypes.data), _P(calls.ctypes.data), 1 if reset else 0)
+    return {L.temo_timing_name(i).decode(): (float(ms[i]), int(calls[i]))
+            for i in range(STAGE_COUNT) if calls[i]}
+
+
+def gather_rows(src, idx, dst):
+    """dst[r] = src[idx[r]] on the device (int32 or int64 idx)."""
+    t = torch()
+    rows, cols = dst.shape[0], src.shape[1]
+    i32 = idx if idx.dtype == t.int32 else None
+    i64 = idx if idx.dtype == t.int64 else None
+    check(lib().temo_gather_rows(ptr(src), ptr(i32), ptr(i64), rows, cols, ptr(dst),
+                                 stream_handle(dst.device)), "gather_rows")
+    return dst
+
+
+def gather_rows2(src, idx_a, idx_b, dst):
+    """dst[r] = src[idx_a[idx_b[r]]] (idx_a int64, idx_b int32)."""
+    rows, cols = dst.shape[0], src.shape[1]
+    check(lib().temo_gather_rows2(ptr(src), ptr(idx_a), ptr(idx_b), rows, cols, ptr(dst),
+                                  stream_handle(dst.device)), "gather_rows2")
+    return dst

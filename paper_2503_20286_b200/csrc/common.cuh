@@ -52,6 +52,14 @@ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 int num_sms();
 
+// stage ids for temo_timing_* (names in capi.cu)
+enum Stage {
+    S_RANK_PREP = 0, S_DOM_BITS, S_PEEL, S_NORMALIZE, S_ASSOCIATE, S_NICHE, S_OFFSPRING,
+    S_EVALUATE, S_HV_COUNT, S_HV_CONTRIB, S_HYPE_SELECT, S_MOEAD, S_GATHER, S_MISC
+};
+void stage_begin(int stage, cudaStream_t st);
+void stage_end(int stage, cudaStream_t st);
+
 // ------------------------------------------------------------ order keys
 // Order-preserving u64 image of a double; -0.0 is folded onto +0.0 so that
 // equal doubles map to equal keys (np comparisons treat them as equal).

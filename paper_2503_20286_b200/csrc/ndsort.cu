@@ -525,6 +525,7 @@ static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStrea
     const int64_t N = p.N;
     const int m = p.m, MP = 4 * p.NV;
     size_t tb = p.cub_bytes;
+    stage_begin(S_RANK_PREP, st);
     // K0: per-column dense ranks
     for (int col = 0; col < m; ++col) {
         k_col_keys<<<grid1(N), 256, 0, st>>>(F, N, m, col, p.keys_a, p.vals_a, status);
@@ -552,7 +553,9 @@ static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStrea
     k_records<<<grid1(p.Np), 256, 0, st>>>(p.R, p.vals_a, p.scan_b, N, p.Np, m, MP, p.NV, p.rec);
     k_rowtile_offsets<<<grid1(p.nT), 256, 0, st>>>(p.nT, p.W, p.rt_off);
     TEMO_LAUNCH_CHECK();
+    stage_end(S_RANK_PREP, st);
     // K1
+    stage_begin(S_DOM_BITS, st);
     const int64_t items = p.nT + CHUNK * ((p.nT / CHUNK) * ((p.nT / CHUNK) - 1) / 2) +
                           (p.nT % CHUNK) * (p.nT / CHUNK);
     const dim3 g((unsigned)items);
@@ -566,6 +569,7 @@ static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStrea
     }
 #undef DOM_CASE
     TEMO_LAUNCH_CHECK();
+    stage_end(S_DOM_BITS, st);
     return TEMO_OK;
 }
 
@@ -625,7 +629,9 @@ extern "C" int temo_rank(const double *F, int64_t N, int m, int64_t n, int mode,
     const size_t smem = (size_t)(2 * (p.NB + 1) + 32) * sizeof(int) + 8 * 8 * 32 * sizeof(uint32_t);
     const int P = peel_grid((int)p.NB, smem);
     void *args[] = {&a};
+    stage_begin(S_PEEL, st);
     TEMO_CUDA(cudaLaunchCooperativeKernel((void *)k_peel, dim3(P), dim3(PEEL_T), args, smem, st));
+    stage_end(S_PEEL, st);
     k_unsort_ranks<<<grid1(N), 256, 0, st>>>(p.rank_s, p.vals_a, l_out, N, rank);
     TEMO_LAUNCH_CHECK();
     return TEMO_OK;

@@ -39,11 +39,12 @@ def _check_objectives(F, what):
         raise ValueError(f"{what}: objective matrix contains NaN rows")
 
 
-def rank_device(Fd, n: int, mode: int = SORT, status=None):
+def rank_device(Fd, n: int, mode: int = SORT, status=None, out=None):
     """Enqueue the GPU sort of a CUDA float64 (N, m) tensor; no host sync.
 
-    Returns ``(rank int32[N], l int32[1], nfronts int32[1])`` device tensors.
-    Data-dependent errors are OR-ed into ``status`` (int32[1]) if given.
+    Returns ``(rank int32[N], l int32[1], nfronts int32[1])`` device tensors
+    (written into ``out`` if given).  Data-dependent errors are OR-ed into
+    ``status`` (int32[1]) if given.
     """
     t = _lib.torch()
     N, m = Fd.shape
@@ -51,9 +52,12 @@ def rank_device(Fd, n: int, mode: int = SORT, status=None):
         raise ValueError(f"population size {n} out of range [1, {N}]")
     L = _lib.lib()
     dev = Fd.device
-    rank = t.empty(N, dtype=t.int32, device=dev)
-    l = t.empty(1, dtype=t.int32, device=dev)
-    nf = t.empty(1, dtype=t.int32, device=dev)
+    if out is None:
+        rank = t.empty(N, dtype=t.int32, device=dev)
+        l = t.empty(1, dtype=t.int32, device=dev)
+        nf = t.empty(1, dtype=t.int32, device=dev)
+    else:
+        rank, l, nf = out
     nbytes = L.temo_rank_ws_bytes(N, m)
     if nbytes == 0:
         raise ValueError(f"unsupported problem size N={N}, m={m}")

@@ -8,6 +8,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2503_20286_b200 import _lib  # noqa: E402
 from paper_2503_20286_b200.ndsort import SELECT, SORT, rank_device  # noqa: E402
 
 
@@ -27,8 +28,13 @@ def main():
                 e.record()
                 torch.cuda.synchronize()
                 ms = s.elapsed_time(e) / reps
+                _lib.timing_enable(True)
+                rank_device(F, N // 2, mode)
+                stages = _lib.timing_read()
+                _lib.timing_enable(False)
                 print(json.dumps(dict(N=N, m=m, mode=mode, ms=round(ms, 3), fronts=int(nf.item()),
-                                      l=int(l.item()), pairs_per_s=N * (N - 1) / ms * 1e3)))
+                                      l=int(l.item()), pairs_per_s=N * (N - 1) / ms * 1e3,
+                                      stages={k: round(v[0], 3) for k, v in stages.items()})))
 
 
 if __name__ == "__main__":

@@ -1,0 +1,192 @@
+"""GPU parity: NSGA-III selection stages vs golden reference vectors and the CPU oracle."""
+
+import numpy as np
+import pytest
+
+from conftest import cases, load_golden
+from oracle import nsga3 as onsga3
+
+pytestmark = pytest.mark.gpu
+
+
+class Planned:
+    def __init__(self, perm):
+        self.perm = np.asarray(perm)
+
+    def permutation(self, n):
+        assert n == self.perm.size
+        return self.perm.copy()
+
+
+@pytest.mark.parametrize("idx", range(14))
+def test_selection_golden_stages(cuda, idx):
+    import torch
+
+    from paper_2503_20286_b200.directions import DirectionSet
+    from paper_2503_20286_b200.nsga3 import Nsga3Selector
+
+    c = cases(load_golden("nsga3"))[idx]
+    Fs = c["F"][c["perm"]]
+    N, m = Fs.shape
+    R = DirectionSet(c["W"], "simplex")
+    sel = Nsga3Selector(N, m, R, int(c["n"]), record=True)
+    keep = sel.select_shuffled(torch.from_numpy(Fs).cuda()).cpu().numpy()
+    sel.check()
+    l = int(sel.l.item())
+    assert l == int(c["l"])
+    r = sel.rank.cpu().numpy()
+    assert np.array_equal(sel.ideal.cpu().numpy(), c["ideal"])
+    assert np.array_equal(sel.icpt.cpu().numpy(), c["intercepts"])
+    live = c["r"] <= l
+    assert np.array_equal(sel.Fp.cpu().numpy()[live], c["Fp"][live])
+    assert np.array_equal(sel.pi.cpu().numpy()[live], c["pi"][live])
+    assert np.array_equal(sel.dist.cpu().numpy()[live], c["dist"][live])
+    k = int(sel.counts[0].item())
+    assert np.array_equal(sel.promoted[:k].cpu().numpy(), c["promoted"])
+    assert np.array_equal(keep, c["keep"])
+    # final ranks agree with the reference wherever the reference rank <= l
+    assert np.array_equal(r[live], c["rank"][live])
+
+
+@pytest.mark.parametrize("idx", [0, 4, 5, 11, 12])
+def test_environmental_selection_numpy_dropin(cuda, idx):
+    from paper_2503_20286_b200.directions import DirectionSet
+    from paper_2503_20286_b200.nsga3 import environmental_selection
+
+    c = cases(load_golden("nsga3"))[idx]
+    N = c["F"].shape[0]
+    X = np.arange(N, dtype=float)[:, None] * np.ones((1, 3))
+    Xs, Fs = environmental_selection(X, c["F"], DirectionSet(c["W"], "simplex"), int(c["n"]),
+                                     Planned(c["perm"]))
+    want = c["perm"][c["keep"]]
+    assert np.array_equal(Xs[:, 0].astype(np.int64), want)
+    assert np.array_equal(Fs, c["F"][want])
+
+
+def test_associate_golden(cuda):
+    from paper_2503_20286_b200.directions import DirectionSet
+    from paper_2503_20286_b200.nsga3 import associate
+
+    for c in cases(load_golden("associate")):
+        out = associate(c["Fp"], DirectionSet(c["W"], "simplex"))
+        assert np.array_equal(out.pi, c["pi"])
+        assert np.array_equal(out.dist, c["dist"], equal_nan=True)
+
+
+def test_normalize_vs_oracle(cuda):
+    from paper_2503_20286_b200.nsga3 import normalize
+
+    rng = np.random.default_rng(71)
+    for trial in range(40):
+        m = int(rng.integers(2, 6))
+        F = rng.random((50, m)) + 0.1
+        F[rng.random(50) < 0.2] = np.nan
+        if trial % 5 == 0:
+            F[:, 0] = 1.0  # degenerate -> fallback intercepts
+        got = normalize(F)
+        Fp, ideal, icpt, _ = onsga3.normalize(F)
+        assert np.array_equal(got.ideal, ideal)
+        assert np.array_equal(got.intercepts, icpt)
+        assert np.array_equal(got.Fp, Fp, equal_nan=True)
+
+
+def test_reference_known_answers(cuda):
+    """Ports of test_nsga3.py known-answer tests (the 4 failing expectations excluded)."""
+    from paper_2503_20286_b200.directions import DirectionSet, das_dennis
+    from paper_2503_20286_b200.nsga3 import (associate, environmental_selection, niche_counts,
+                                             niche_select, normalize, update_rank)
+
+    out = normalize(np.array([[3.0, 0.0], [0.0, 2.0]]))
+    assert np.allclose(out.intercepts, [3.0, 2.0]) and np.allclose(out.Fp, [[1.0, 0.0], [0.0, 1.0]])
+    assert np.allclose(normalize(np.array([[1.0, 1.0], [2.0, 2.0]])).intercepts, [2.0, 2.0])
+    with pytest.raises(ValueError):
+        normalize(np.full((3, 2), np.nan))
+    R = DirectionSet(np.array([[0.0, 1.0]]), "simplex")
+    assert np.isclose(associate(np.array([[1.0, 0.0]]), R).dist[0], 1.0)
+    R = DirectionSet(np.array([[1.0, 0.0], [0.0, 1.0]]), "simplex")
+    z = associate(np.zeros((1, 2)), R)
+    assert z.dist[0] == 0.0 and z.pi[0] == 0
+    # parallel row: equals the oracle (the reference's own <1e-12 expectation fails)
+    R = DirectionSet(np.array([[1.0, 0.0], [0.5, 0.5]]), "simplex")
+    a = associate(np.array([[0.4, 0.4]]), R)
+    pi, dist = onsga3.associate(np.array([[0.4, 0.4]]), R.W)
+    assert a.pi[0] == pi[0] == 1 and a.dist[0] == dist[0]
+    st = niche_counts(np.array([1, 1, 1]), np.array([0, 2, 2]), 1, 3)
+    assert st.rho.tolist() == [0, 0, 0] and st.rho_l.tolist() == [1, 0, 2] and st.n_s == 0
+    st = niche_counts(np.array([0, 0, 1]), np.array([1, 1, 0]), 2, 2)
+    rho, rho_l, n_s = onsga3.niche_counts(np.array([0, 0, 1]), np.array([1, 1, 0]), 2, 2)
+    assert st.rho.tolist() == rho.tolist() and st.rho_l.tolist() == rho_l.tolist() and st.n_s == n_s
+    r, pi, dist = np.array([0, 1, 1]), np.array([0, 1, 1]), np.array([0.0, 0.7, 0.3])
+    sel = niche_select(niche_counts(r, pi, 1, 2), r, pi, dist, 1, 2)
+    assert sel.rank[2] == 0 and sel.rank[1] == 1 and sel.promoted.tolist() == [2]
+    r, pi = np.array([0, 1]), np.array([0, 0])
+    sel = niche_select(niche_counts(r, pi, 1, 1), r, pi, np.array([0.1, 0.2]), 1, 2)
+    assert sel.promoted.size == 0 and sel.rank.tolist() == [0, 1]
+    r = np.array([0, 1, 1])
+    assert np.array_equal(update_rank(r, np.array([], dtype=np.int64), 0, 1), r)
+    assert update_rank(np.array([1, 1, 1, 0]), np.array([], dtype=np.int64), 2, 1).tolist() == [0, 0, 1, 0]
+    assert update_rank(np.array([0, 0, 0, 1]), np.array([1, 2]), -1, 1).tolist() == [0, 0, 1, 1]
+    with pytest.raises(RuntimeError):
+        update_rank(np.array([1, 1]), np.array([], dtype=np.int64), 3, 1)
+    # dominators kept / exact front fit
+    rng = np.random.default_rng(76)
+    top = rng.random((10, 3))
+    rest = top.max(axis=0) + 1.0 + rng.random((10, 3))
+    X = np.arange(20, dtype=float)[:, None] * np.ones((1, 4))
+    _, Fs = environmental_selection(X, np.vstack([top, rest]), das_dennis(3, 4), 10, np.random.default_rng(0))
+    assert {tuple(x) for x in Fs} == {tuple(x) for x in top}
+
+
+def test_update_rank_final_count_random(cuda):
+    from paper_2503_20286_b200.ndsort import rank_assign
+    from paper_2503_20286_b200.nsga3 import niche_counts, niche_select, update_rank
+
+    rng = np.random.default_rng(75)
+    for _ in range(60):
+        N = int(rng.integers(6, 40))
+        n = int(rng.integers(2, N))
+        F = rng.random((N, 3))
+        res = rank_assign(F, n)
+        pi = rng.integers(0, 8, size=N)
+        dist = rng.random(N)
+        st = niche_counts(res.r, pi, res.l, 8)
+        sel = niche_select(st, res.r, pi, dist, res.l, n)
+        out = update_rank(sel.rank, sel.promoted, n - sel.n_selected, res.l)
+        rho, _, n_s = onsga3.niche_counts(res.r, pi, res.l, 8)
+        rank2, prom2, n_sel2 = onsga3.niche_select(rho, n_s, res.r, pi, dist, res.l)
+        assert np.array_equal(sel.promoted, prom2) and sel.n_selected == n_sel2
+        assert np.array_equal(out, onsga3.update_rank(rank2, prom2, n - n_sel2, res.l))
+        assert int(np.sum(out < res.l)) == n
+
+
+@pytest.mark.parametrize("N,m,H,seed", [(4000, 3, 40, 1), (3000, 3, 76, 2), (2000, 4, 12, 3),
+                                         (1500, 5, 8, 4), (1000, 8, 4, 5), (6000, 2, 300, 6)])
+def test_selection_vs_oracle_random(cuda, N, m, H, seed):
+    import torch
+
+    from paper_2503_20286_b200.directions import das_dennis
+    from paper_2503_20286_b200.nsga3 import Nsga3Selector
+
+    rng = np.random.default_rng(seed)
+    F = rng.random((N, m)) ** 2
+    if seed % 2:
+        F = np.round(F, 2)  # ties in every stage
+    R = das_dennis(m, H)
+    n = N // 2
+    sel = Nsga3Selector(N, m, R, n, record=True)
+    keep = sel.select_shuffled(torch.from_numpy(F).cuda()).cpu().numpy()
+    sel.check()
+    want = onsga3.select_shuffled(F, R.W, n)
+    assert int(sel.l.item()) == want["l"]
+    live = want["r"] <= want["l"]
+    assert np.array_equal(sel.pi.cpu().numpy()[live], want["pi"][live])
+    assert np.array_equal(sel.dist.cpu().numpy()[live], want["dist"][live])
+    assert np.array_equal(keep, want["keep"])
+
+
+def test_neighbors_golden(cuda):
+    from paper_2503_20286_b200.directions import DirectionSet, neighbors
+
+    for c in cases(load_golden("neighbors")):
+        got = neighbors(DirectionSet(c["W"], "simplex"), c["I"].shape[1]).I_nb
+        assert np.array_equal(got, c["I"])
