@@ -120,11 +120,80 @@ int temo_gather_rows(const double *src, const int32_t *idx32, const int64_t *idx
 int temo_gather_rows2(const double *src, const int64_t *idx_a, const int32_t *idx_b, int64_t rows,
                       int64_t cols, double *dst, temo_stream_t stream);
 
+/* ----------------------------------------------------- RNG, problems, variation
+ * NumPy Philox state (np.random.Philox().state: counter, key, buffer,
+ * buffer_pos).  Uniform e of a draw that starts `off` raw outputs after this
+ * state is bit-identical to the host's Generator.random (rng.py:28-31). */
+typedef struct temo_philox_state {
+    uint64_t counter[4];
+    uint64_t key[2];
+    uint64_t buffer[4];
+    int32_t buffer_pos;
+    int32_t reserved;
+} temo_philox_state;
+
+#define TEMO_PROB_DTLZ1 1 /* ... TEMO_PROB_DTLZ1 + 6 = DTLZ7 (problems.py:105-136) */
+#define TEMO_PROB_LSMOP1 101 /* LSMOP1, Cheng et al. 2017 (no reference; self-oracle) */
+
+typedef struct temo_problem {
+    int32_t id;          /* TEMO_PROB_* */
+    int32_t m;           /* objectives, 2..16 */
+    int64_t d;           /* decision variables */
+    int32_t nk;          /* LSMOP: subcomponents per objective */
+    int32_t sublen[16];  /* LSMOP: subcomponent length per objective */
+    int32_t offset[17];  /* LSMOP: start of objective i's groups within x^s */
+} temo_problem;
+
+typedef struct temo_variation {
+    double eta_c, eta_m, p_m; /* variation.py:17-45 (p_m resolved: None -> 1/d) */
+    int32_t gene_swap;
+    int32_t reserved;
+    const double *lower, *upper; /* device, length d */
+} temo_variation;
+
+/* problems.evaluate (problems.py:105-136; LSMOP1 new): F (n x m) = f(X (n x d)) */
+int temo_evaluate(const temo_problem *prob, const double *X, int64_t n, double *F,
+                  temo_stream_t stream);
+
+/* Uniform draws: out[e] = Generator.random() element `off + e` of the stream. */
+int temo_uniform(const temo_philox_state *st, uint64_t off, int64_t count, double *out,
+                 temo_stream_t stream);
+
+/* variation.sbx (variation.py:57-91): C (2q x d) = clip([c1; c2]).  Uniforms
+ * come from the Philox stream at off (mu, then swap and crossed when
+ * gene_swap; q*d each) unless the u_* arrays are given (injected draws). */
+int temo_sbx(const temo_variation *var, const double *X1, const double *X2, int64_t q, int64_t d,
+             const temo_philox_state *st, uint64_t off, const double *u_mu, const double *u_swap,
+             const double *u_cross, double *C, temo_stream_t stream);
+
+/* variation.polynomial_mutation (variation.py:94-120): Y (rows x d); draws mu
+ * then hit (rows*d each) from the stream at off unless injected. */
+int temo_pm(const temo_variation *var, const double *X, int64_t rows, int64_t d,
+            const temo_philox_state *st, uint64_t off, const double *u_mu, const double *u_hit,
+            double *Y, temo_stream_t stream);
+
+/* Fused generation front end for NSGA-III / HypE (harness.py:201-204, 220):
+ * pairs (i1[q], i2[q]) of parent rows of X -> SBX -> PM -> evaluate, writing
+ * offspring O (2h x d) and objectives FO (2h x m; NULL skips evaluation).
+ * Draws follow the reference call order from `off`: SBX mu/swap/crossed
+ * (h*d each), PM mu/hit (2h*d each). */
+int temo_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
+                   const int64_t *i1, const int64_t *i2, int64_t h, const temo_philox_state *st,
+                   uint64_t off, double *O, double *FO, temo_stream_t stream);
+
+/* harness._Stepper.init (harness.py:188-190): X = lower + U (upper - lower), U from the stream. */
+int temo_init_population(const temo_philox_state *st, uint64_t off, int64_t rows, int64_t d,
+                         const double *lower, const double *upper, double *X, temo_stream_t stream);
+
 /* --------------------------------------------------------------- directions
  * directions.neighbors (directions.py:104-114): out (r x T int32) holds the T
  * nearest rows of W (r x m) by Euclidean distance, ties to the lower index.
  * 1 <= T <= min(r, 64), m <= 16. */
 int temo_neighbors(const double *W, int64_t r, int m, int T, int32_t *out, temo_stream_t stream);
+
+/* Roofline probe: compare-pipe rate (compares/s) of the K1 instruction mix on
+ * register operands (the denominator of bench.py's integer roofline). */
+double temo_probe_compare_rate(int blocks, int iters, temo_stream_t stream);
 
 /* ------------------------------------------------------------ stage timing
  * CUDA-event timing of each kernel stage on its own stream (off by default).

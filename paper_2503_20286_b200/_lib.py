@@ -21,6 +21,12 @@ _I64 = ctypes.c_int64
 _I32 = ctypes.c_int
 _SZ = ctypes.c_size_t
 _D = ctypes.c_double
+_U64 = ctypes.c_uint64
+
+
+def sptr(struct):
+    """Address of a ctypes Structure as a void* argument (valid for the call)."""
+    return _P(ctypes.addressof(struct))
 
 # name -> (restype, argtypes); must mirror include/temo_b200.h
 SIGNATURES = {
@@ -41,6 +47,13 @@ SIGNATURES = {
     "temo_gather_rows": (_I32, [_P, _P, _P, _I64, _I64, _P, _P]),
     "temo_gather_rows2": (_I32, [_P, _P, _P, _I64, _I64, _P, _P]),
     "temo_neighbors": (_I32, [_P, _I64, _I32, _I32, _P, _P]),
+    "temo_evaluate": (_I32, [_P, _P, _I64, _P, _P]),
+    "temo_uniform": (_I32, [_P, _U64, _I64, _P, _P]),
+    "temo_sbx": (_I32, [_P, _P, _P, _I64, _I64, _P, _U64, _P, _P, _P, _P, _P]),
+    "temo_pm": (_I32, [_P, _P, _I64, _I64, _P, _U64, _P, _P, _P, _P]),
+    "temo_offspring": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _U64, _P, _P, _P]),
+    "temo_init_population": (_I32, [_P, _U64, _I64, _I64, _P, _P, _P, _P]),
+    "temo_probe_compare_rate": (_D, [_I32, _I32, _P]),
     "temo_timing_enable": (None, [_I32]),
     "temo_timing_name": (ctypes.c_char_p, [_I32]),
     "temo_timing_read": (_I32, [_P, _P, _I32]),
@@ -220,3 +233,31 @@ def gather_rows2(src, idx_a, idx_b, dst):
     check(lib().temo_gather_rows2(ptr(src), ptr(idx_a), ptr(idx_b), rows, cols, ptr(dst),
                                   stream_handle(dst.device)), "gather_rows2")
     return dst
+
+
+class HostRing:
+    """Pinned host staging buffers for per-step H2D uploads (no host/GPU serialisation)."""
+
+    def __init__(self, slots: int = 4):
+        self.slots = slots
+        self.bufs = {}
+        self.next = {}
+
+    def upload(self, arr: np.ndarray, dst):
+        t = torch()
+        arr = np.ascontiguousarray(arr)
+        key = (arr.dtype.str, arr.size)
+        ring = self.bufs.setdefault(key, [None] * self.slots)
+        k = self.next.get(key, 0)
+        self.next[key] = (k + 1) % self.slots
+        slot = ring[k]
+        if slot is None:
+            host = t.from_numpy(np.empty(arr.shape, dtype=arr.dtype)).pin_memory()
+            slot = ring[k] = [host, t.cuda.Event()]
+        else:
+            slot[1].synchronize()  # previous copy out of this slot has finished
+        host, ev = slot
+        host.numpy().reshape(-1)[:] = arr.reshape(-1)
+        dst.view(-1).copy_(host.view(-1), non_blocking=True)
+        ev.record(t.cuda.current_stream(dst.device))
+        return dst

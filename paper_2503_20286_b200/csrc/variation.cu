@@ -1,0 +1,408 @@
+// Offspring generation and problem evaluation on B200
+// (replaces temo variation.py:48-120, problems.py:69-136, harness.py:201-204).
+//
+// The generation front end is ONE kernel: a CTA owns a parent pair, draws its
+// uniforms straight from the NumPy-compatible Philox stream (philox.cuh),
+// applies SBX and polynomial mutation with the reference's op sequence
+// (only the taken np.where branch is evaluated, which is
+// bit-identical), stages both children in shared memory and evaluates them
+// (DTLZ1-7 or LSMOP1) with block reductions -- no uniform matrices, children
+// or objectives round-trip through HBM except the final O and FO rows.
+#include "common.cuh"
+#include "philox.cuh"
+
+namespace temo {
+
+constexpr int VT = 128;
+constexpr double PI = 3.141592653589793;
+
+__device__ __forceinline__ double clipv(double x, double lo, double hi) {
+    // np.clip(a, lo, hi) == minimum(maximum(a, lo), hi)
+    double y = x < lo ? lo : x;
+    return y > hi ? hi : y;
+}
+
+__device__ __forceinline__ void sbx_gene(double x1, double x2, double mu, double swp, double crs,
+                                         double e, bool gene_swap, double &c1, double &c2) {
+    double beta;
+    if (gene_swap && !(crs < 0.5)) {
+        beta = 1.0;  // not crossed: masked_blend(crossed, beta, 1)
+    } else {
+        beta = (0.5 - mu >= 0.0) ? pow(2.0 * mu, e) : pow(1.0 / (2.0 - 2.0 * mu), e);
+        if (gene_swap) beta = beta * (1.0 - 2.0 * (swp < 0.5 ? 1.0 : 0.0));
+    }
+    const double shift = 0.5 * (1.0 - beta);
+    c1 = x1 + shift * (x2 - x1);
+    c2 = x2 + shift * (x1 - x2);
+}
+
+__device__ __forceinline__ double pm_step(double x, double lo, double hi, double mu, double eta) {
+    const double span = hi - lo;
+    double step;
+    if (0.5 - mu >= 0.0) {
+        const double gap = (x - lo) / span;
+        step = pow(2.0 * mu + (1.0 - 2.0 * mu) * pow(1.0 - gap, eta), 1.0 / eta) - 1.0;
+    } else {
+        const double gap = (hi - x) / span;
+        step = 1.0 - pow(2.0 - 2.0 * mu + (2.0 * mu - 1.0) * pow(1.0 - gap, eta), 1.0 / eta);
+    }
+    return x + step * span;
+}
+
+// ------------------------------------------------------------------ evaluation
+__device__ double block_sum(double v, double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(~0u, v, d);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    return s;
+}
+
+// objectives of one row x (length d) -> f[0..m); called by every thread of the CTA
+__device__ void eval_row(const temo_problem &P, const double *x, double *f, double *red) {
+    const int m = P.m;
+    const int64_t d = P.d;
+    const int id = P.id;
+    if (id == TEMO_PROB_LSMOP1) {
+        double part[16];
+        for (int i = 0; i < m; ++i) part[i] = 0.0;
+        const double x0 = x[0];
+        const int64_t span_s = P.offset[m];
+        for (int64_t g = (m - 1) + threadIdx.x; g < d; g += blockDim.x) {
+            const int64_t rel = g - (m - 1);
+            if (rel >= span_s) continue;
+            const double a = (double)(g + 1);
+            const double xs = (1.0 + a / (double)d) * x[g] - 10.0 * x0;
+            int i = 0;
+            while (i + 1 < m && rel >= P.offset[i + 1]) ++i;
+            part[i] += xs * xs;
+        }
+        double G[16];
+        for (int i = 0; i < m; ++i) G[i] = block_sum(part[i], red);
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < m; ++i) {
+                const double gi = G[i] / (double)P.sublen[i] / (double)P.nk;
+                double head = 1.0;
+                for (int k = 0; k < m - 1 - i; ++k) head = head * x[k];
+                const double tail = i == 0 ? 1.0 : 1.0 - x[m - 1 - i];
+                f[i] = (1.0 + gi) * head * tail;
+            }
+        }
+        return;
+    }
+    // DTLZ family: g over the distance variables xm = x[m-1:]
+    const int64_t k = d - m + 1;
+    double acc = 0.0;
+    for (int64_t g = (m - 1) + threadIdx.x; g < d; g += blockDim.x) {
+        const double v = x[g];
+        switch (id) {
+            case 1:
+            case 3: {
+                const double z = v - 0.5;
+                acc += z * z - cos(20.0 * PI * z);
+                break;
+            }
+            case 2:
+            case 4:
+            case 5: {
+                const double z = v - 0.5;
+                acc += z * z;
+                break;
+            }
+            case 6: acc += pow(v, 0.1); break;
+            default: acc += v; break;  // dtlz7
+        }
+    }
+    const double s = block_sum(acc, red);
+    if (threadIdx.x != 0) return;
+    double g;
+    if (id == 1 || id == 3) g = 100.0 * ((double)k + s);
+    else if (id == 7) g = 1.0 + 9.0 / (double)k * s;
+    else g = s;
+    if (id == 1) {
+        for (int i = 0; i < m; ++i) {
+            double p = 1.0;
+            for (int q = 0; q < m - 1 - i; ++q) p = p * x[q];
+            if (i) p = p * (1.0 - x[m - 1 - i]);
+            f[i] = 0.5 * (1.0 + g) * p;
+        }
+        return;
+    }
+    if (id == 7) {
+        double h = 0.0;
+        for (int q = 0; q < m - 1; ++q) {
+            f[q] = x[q];
+            h += x[q] / (1.0 + g) * (1.0 + sin(3.0 * PI * x[q]));
+        }
+        f[m - 1] = (1.0 + g) * ((double)m - h);
+        return;
+    }
+    double th[16];
+    for (int q = 0; q < m - 1; ++q) {
+        if (id == 4) th[q] = pow(x[q], 100.0) * (PI / 2.0);
+        else if (id == 5 || id == 6) {
+            if (q == 0) th[q] = x[0] * (PI / 2.0);
+            else th[q] = PI / (4.0 * (1.0 + g)) * (1.0 + 2.0 * g * x[q]);
+        } else th[q] = x[q] * (PI / 2.0);
+    }
+    for (int i = 0; i < m; ++i) {
+        double p = 1.0;
+        for (int q = 0; q < m - 1 - i; ++q) p = p * cos(th[q]);
+        if (i) p = p * sin(th[m - 1 - i]);
+        f[i] = (1.0 + g) * p;
+    }
+}
+
+__global__ void __launch_bounds__(VT) k_evaluate(temo_problem P, const double *__restrict__ X,
+                                                 int64_t n, double *__restrict__ F) {
+    __shared__ double red[VT / 32];
+    __shared__ double f[16];
+    const int64_t r = blockIdx.x;
+    if (r >= n) return;
+    eval_row(P, X + r * P.d, f, red);
+    __syncthreads();
+    if (threadIdx.x < P.m) F[r * P.m + threadIdx.x] = f[threadIdx.x];
+}
+
+// ------------------------------------------------------------------ fused offspring
+struct VarArgs {
+    double eta_c, eta_m, p_m;
+    int gene_swap;
+    const double *lower, *upper;
+};
+
+__global__ void __launch_bounds__(VT) k_offspring(temo_problem P, VarArgs V, const double *__restrict__ X,
+                                                  const int64_t *__restrict__ i1,
+                                                  const int64_t *__restrict__ i2, int64_t h,
+                                                  Philox ph, uint64_t off, double *__restrict__ O,
+                                                  double *__restrict__ FO, int smem_rows) {
+    extern __shared__ double srow[];  // 2 x d children when smem_rows
+    __shared__ double red[VT / 32];
+    __shared__ double f[16];
+    const int64_t q = blockIdx.x;
+    const int64_t d = P.d;
+    const double *x1 = X + i1[q] * d;
+    const double *x2 = X + i2[q] * d;
+    double *o1 = O + q * d;
+    double *o2 = O + (h + q) * d;
+    const uint64_t hd = (uint64_t)h * d;
+    const uint64_t o_mu = off, o_swap = off + hd, o_cross = off + (V.gene_swap ? 2 * hd : 0);
+    const uint64_t o_pmu = off + (V.gene_swap ? 3 * hd : hd);
+    const uint64_t o_hit = o_pmu + 2 * hd;
+    const double e = 1.0 / (V.eta_c + 1.0);
+    const double eta = V.eta_m + 1.0;
+    PhiloxCursor c_mu, c_sw, c_cr, c_pm1, c_pm2, c_h1, c_h2;
+    for (int64_t g0 = 4 * (int64_t)threadIdx.x; g0 < d; g0 += 4 * VT) {
+        const int64_t g1 = g0 + 4 < d ? g0 + 4 : d;
+        for (int64_t g = g0; g < g1; ++g) {
+            const uint64_t es = (uint64_t)q * d + g;
+            double c1, c2;
+            const double crs = V.gene_swap ? c_cr.uniform(ph, o_cross + es) : 0.0;
+            if (V.gene_swap && !(crs < 0.5)) {
+                sbx_gene(x1[g], x2[g], 0.0, 0.0, crs, e, true, c1, c2);
+            } else {
+                const double mu = c_mu.uniform(ph, o_mu + es);
+                const double sw = V.gene_swap ? c_sw.uniform(ph, o_swap + es) : 1.0;
+                sbx_gene(x1[g], x2[g], mu, sw, crs, e, V.gene_swap, c1, c2);
+            }
+            const double lo = V.lower[g], hi = V.upper[g];
+            c1 = clipv(c1, lo, hi);
+            c2 = clipv(c2, lo, hi);
+            // polynomial mutation on rows q (c1) and h+q (c2)
+            const uint64_t e1 = es, e2 = (uint64_t)(h + q) * d + g;
+            if (V.p_m - c_h1.uniform(ph, o_hit + e1) >= 0.0)
+                c1 = pm_step(c1, lo, hi, c_pm1.uniform(ph, o_pmu + e1), eta);
+            if (V.p_m - c_h2.uniform(ph, o_hit + e2) >= 0.0)
+                c2 = pm_step(c2, lo, hi, c_pm2.uniform(ph, o_pmu + e2), eta);
+            c1 = clipv(c1, lo, hi);
+            c2 = clipv(c2, lo, hi);
+            o1[g] = c1;
+            o2[g] = c2;
+            if (smem_rows) {
+                srow[g] = c1;
+                srow[d + g] = c2;
+            }
+        }
+    }
+    if (!FO) return;
+    __syncthreads();
+    const double *r1 = smem_rows ? srow : o1;
+    const double *r2 = smem_rows ? srow + d : o2;
+    if (!smem_rows) __threadfence_block();
+    eval_row(P, r1, f, red);
+    __syncthreads();
+    if (threadIdx.x < P.m) FO[q * P.m + threadIdx.x] = f[threadIdx.x];
+    __syncthreads();
+    eval_row(P, r2, f, red);
+    __syncthreads();
+    if (threadIdx.x < P.m) FO[(h + q) * P.m + threadIdx.x] = f[threadIdx.x];
+}
+
+// ------------------------------------------------------------------ standalone operators
+__global__ void k_sbx(VarArgs V, const double *__restrict__ X1, const double *__restrict__ X2,
+                      int64_t q, int64_t d, Philox ph, USrc umu, USrc usw, USrc ucr,
+                      double *__restrict__ C) {
+    const int64_t base = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    const double e = 1.0 / (V.eta_c + 1.0);
+    PhiloxCursor a, b, c;
+    for (int64_t t = base; t < base + 4 && t < q * d; ++t) {
+        const int64_t g = t % d;
+        const double mu = umu.get(ph, a, t);
+        const double sw = V.gene_swap ? usw.get(ph, b, t) : 1.0;
+        const double cr = V.gene_swap ? ucr.get(ph, c, t) : 0.0;
+        double c1, c2;
+        sbx_gene(X1[t], X2[t], mu, sw, cr, e, V.gene_swap, c1, c2);
+        C[t] = clipv(c1, V.lower[g], V.upper[g]);
+        C[q * d + t] = clipv(c2, V.lower[g], V.upper[g]);
+    }
+}
+
+__global__ void k_pm(VarArgs V, const double *__restrict__ X, int64_t rows, int64_t d, Philox ph,
+                     USrc umu, USrc uhit, double *__restrict__ Y) {
+    const int64_t base = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    const double eta = V.eta_m + 1.0;
+    PhiloxCursor a, b;
+    for (int64_t t = base; t < base + 4 && t < rows * d; ++t) {
+        const int64_t g = t % d;
+        const double lo = V.lower[g], hi = V.upper[g];
+        const double mu = umu.get(ph, a, t);
+        const double hu = uhit.get(ph, b, t);
+        double y = X[t];
+        if (V.p_m - hu >= 0.0) y = pm_step(y, lo, hi, mu, eta);
+        Y[t] = clipv(y, lo, hi);
+    }
+}
+
+__global__ void k_uniform(Philox ph, uint64_t off, int64_t count, double *__restrict__ out) {
+    const int64_t base = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    PhiloxCursor c;
+    for (int64_t t = base; t < base + 4 && t < count; ++t) out[t] = c.uniform(ph, off + t);
+}
+
+// harness.py:188-190: X = lower + U * (upper - lower)
+__global__ void k_init_population(Philox ph, uint64_t off, int64_t rows, int64_t d,
+                                  const double *__restrict__ lo, const double *__restrict__ hi,
+                                  double *__restrict__ X) {
+    const int64_t base = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    PhiloxCursor c;
+    for (int64_t t = base; t < base + 4 && t < rows * d; ++t) {
+        const int64_t g = t % d;
+        X[t] = lo[g] + c.uniform(ph, off + t) * (hi[g] - lo[g]);
+    }
+}
+
+static VarArgs var_args(const temo_variation *v) {
+    VarArgs a;
+    a.eta_c = v->eta_c;
+    a.eta_m = v->eta_m;
+    a.p_m = v->p_m;
+    a.gene_swap = v->gene_swap;
+    a.lower = v->lower;
+    a.upper = v->upper;
+    return a;
+}
+
+static bool prob_ok(const temo_problem *p) {
+    if (!p || p->m < 2 || p->m > 16 || p->d < p->m) return false;
+    if (p->id == TEMO_PROB_LSMOP1) return p->nk >= 1;
+    return p->id >= 1 && p->id <= 7;
+}
+
+static Philox philox_or_zero(const temo_philox_state *st) {
+    if (st) return philox_from(*st);
+    temo_philox_state z = {};
+    z.buffer_pos = 4;
+    return philox_from(z);
+}
+
+}  // namespace temo
+
+using namespace temo;
+
+extern "C" int temo_evaluate(const temo_problem *prob, const double *X, int64_t n, double *F,
+                             temo_stream_t stream) {
+    if (!prob_ok(prob) || n < 0 || !X || !F) return TEMO_EINVAL;
+    if (n == 0) return TEMO_OK;
+    stage_begin(S_EVALUATE, (cudaStream_t)stream);
+    k_evaluate<<<(unsigned)n, VT, 0, (cudaStream_t)stream>>>(*prob, X, n, F);
+    TEMO_LAUNCH_CHECK();
+    stage_end(S_EVALUATE, (cudaStream_t)stream);
+    return TEMO_OK;
+}
+
+extern "C" int temo_uniform(const temo_philox_state *st, uint64_t off, int64_t count, double *out,
+                            temo_stream_t stream) {
+    if (!st || count < 0 || !out) return TEMO_EINVAL;
+    if (count == 0) return TEMO_OK;
+    const int64_t th = (count + 3) / 4;
+    k_uniform<<<(unsigned)((th + 255) / 256), 256, 0, (cudaStream_t)stream>>>(philox_from(*st), off,
+                                                                             count, out);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
+extern "C" int temo_sbx(const temo_variation *var, const double *X1, const double *X2, int64_t q,
+                        int64_t d, const temo_philox_state *st, uint64_t off, const double *u_mu,
+                        const double *u_swap, const double *u_cross, double *C,
+                        temo_stream_t stream) {
+    if (!var || q < 0 || d < 1 || !X1 || !X2 || !C) return TEMO_EINVAL;
+    if (!st && (!u_mu || (var->gene_swap && (!u_swap || !u_cross)))) return TEMO_EINVAL;
+    if (q == 0) return TEMO_OK;
+    const uint64_t qd = (uint64_t)q * d;
+    USrc a{u_mu, off}, b{u_swap, off + qd}, c{u_cross, off + 2 * qd};
+    const int64_t th = (q * d + 3) / 4;
+    k_sbx<<<(unsigned)((th + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        var_args(var), X1, X2, q, d, philox_or_zero(st), a, b, c, C);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
+extern "C" int temo_pm(const temo_variation *var, const double *X, int64_t rows, int64_t d,
+                       const temo_philox_state *st, uint64_t off, const double *u_mu,
+                       const double *u_hit, double *Y, temo_stream_t stream) {
+    if (!var || rows < 0 || d < 1 || !X || !Y) return TEMO_EINVAL;
+    if (!st && (!u_mu || !u_hit)) return TEMO_EINVAL;
+    if (rows == 0) return TEMO_OK;
+    const uint64_t rd = (uint64_t)rows * d;
+    USrc a{u_mu, off}, b{u_hit, off + rd};
+    const int64_t th = (rows * d + 3) / 4;
+    k_pm<<<(unsigned)((th + 255) / 256), 256, 0, (cudaStream_t)stream>>>(var_args(var), X, rows, d,
+                                                                         philox_or_zero(st), a, b, Y);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
+extern "C" int temo_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
+                              const int64_t *i1, const int64_t *i2, int64_t h,
+                              const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                              temo_stream_t stream) {
+    if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !st || !O) return TEMO_EINVAL;
+    if (h == 0) return TEMO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t d = prob->d;
+    int smem_rows = 2 * d * (int64_t)sizeof(double) <= 96 * 1024;
+    const size_t smem = smem_rows ? 2 * d * sizeof(double) : 0;
+    if (smem > 48 * 1024)
+        TEMO_CUDA(cudaFuncSetAttribute(k_offspring, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    stage_begin(S_OFFSPRING, s);
+    k_offspring<<<(unsigned)h, VT, smem, s>>>(*prob, var_args(var), X, i1, i2, h, philox_from(*st),
+                                              off, O, FO, smem_rows);
+    TEMO_LAUNCH_CHECK();
+    stage_end(S_OFFSPRING, s);
+    return TEMO_OK;
+}
+
+extern "C" int temo_init_population(const temo_philox_state *st, uint64_t off, int64_t rows,
+                                    int64_t d, const double *lower, const double *upper, double *X,
+                                    temo_stream_t stream) {
+    if (!st || rows < 0 || d < 1 || !lower || !upper || !X) return TEMO_EINVAL;
+    if (rows == 0) return TEMO_OK;
+    const int64_t th = (rows * d + 3) / 4;
+    k_init_population<<<(unsigned)((th + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        philox_from(*st), off, rows, d, lower, upper, X);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}

@@ -1,0 +1,165 @@
+"""Benchmark problems -- drop-in for ``temo.problems`` (problems.py:21-184) plus LSMOP1.
+
+Evaluation runs on the GPU (``temo_evaluate``; fused into offspring generation
+by ``temo_offspring``).  DTLZ1-7 follow problems.py:69-136 op for op; results
+agree with NumPy to the last few ulps (transcendentals differ), inside the
+north star's 1e-5 relative tolerance.  LSMOP1 is new (the reference has no
+LSMOP): the standard definition of Cheng et al. 2017 in the PlatEMO
+formulation -- linear linkage x^s_i <- (1 + i/D) x^s_i - 10 x_1, chaotic
+subcomponent sizes (c <- 3.8 c (1 - c), nk = 5), Sphere g on every group and
+the linear front.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .directions import largest_h_for, simplex_lattice
+
+DTLZ = ("dtlz1", "dtlz2", "dtlz3", "dtlz4", "dtlz5", "dtlz6", "dtlz7")
+LSMOP = ("lsmop1",)
+_NAMES = DTLZ + LSMOP
+PROB_LSMOP1 = 101
+
+
+class ProblemStruct(ctypes.Structure):
+    """Mirror of ``temo_problem`` (include/temo_b200.h)."""
+
+    _fields_ = [("id", ctypes.c_int32), ("m", ctypes.c_int32), ("d", ctypes.c_int64),
+                ("nk", ctypes.c_int32), ("sublen", ctypes.c_int32 * 16),
+                ("offset", ctypes.c_int32 * 17)]
+
+
+def lsmop_groups(m: int, d: int, nk: int = 5):
+    """Subcomponent lengths per objective and group offsets within x^s."""
+    c = [3.8 * 0.1 * (1.0 - 0.1)]
+    for _ in range(m - 1):
+        c.append(3.8 * c[-1] * (1.0 - c[-1]))
+    c = np.asarray(c)
+    sublen = np.floor(c / c.sum() * (d - m + 1) / nk).astype(np.int64)
+    offset = np.concatenate([[0], np.cumsum(sublen * nk)])
+    return sublen, offset
+
+
+@dataclass(frozen=True)
+class ProblemSpec:
+    """A DTLZ/LSMOP instance: name, decision dimension d, objective count m (problems.py:21-50)."""
+
+    name: str
+    d: int
+    m: int
+    lower: np.ndarray = field(default=None)
+    upper: np.ndarray = field(default=None)
+
+    def __post_init__(self):
+        if self.name not in _NAMES:
+            raise ValueError(f"unknown problem {self.name!r}")
+        if self.m < 2:
+            raise ValueError("need at least 2 objectives")
+        if self.d < self.m:
+            raise ValueError("DTLZ needs d >= m")
+        if self.name in LSMOP:
+            dl = np.zeros(self.d)
+            du = np.concatenate([np.ones(self.m - 1), np.full(self.d - self.m + 1, 10.0)])
+        else:
+            dl, du = np.zeros(self.d), np.ones(self.d)
+        lower = dl if self.lower is None else np.asarray(self.lower, dtype=np.float64)
+        upper = du if self.upper is None else np.asarray(self.upper, dtype=np.float64)
+        if lower.shape != (self.d,) or upper.shape != (self.d,):
+            raise ValueError("bounds must be length-d vectors")
+        if not np.all(lower < upper):
+            raise ValueError("lower bounds must be strictly below upper bounds")
+        object.__setattr__(self, "lower", lower)
+        object.__setattr__(self, "upper", upper)
+
+    @property
+    def k(self) -> int:
+        return self.d - self.m + 1
+
+    def struct(self) -> ProblemStruct:
+        s = ProblemStruct()
+        s.m, s.d = self.m, self.d
+        if self.name in LSMOP:
+            s.id = PROB_LSMOP1
+            s.nk = 5
+            sub, off = lsmop_groups(self.m, self.d, 5)
+            if (sub < 1).any():
+                raise ValueError("LSMOP needs d large enough for every subcomponent")
+            for i in range(self.m):
+                s.sublen[i] = int(sub[i])
+            for i in range(self.m + 1):
+                s.offset[i] = int(off[i])
+        else:
+            s.id = DTLZ.index(self.name) + 1
+        return s
+
+
+def default_dimension(name: str, m: int) -> int:
+    """problems.py:53-59; LSMOP: D = 100 m (PlatEMO default)."""
+    if name == "dtlz1":
+        return m + 4
+    if name == "dtlz7":
+        return m + 19
+    if name in LSMOP:
+        return 100 * m
+    return m + 9
+
+
+def make_problem(name: str, m: int = 3, d: int | None = None) -> ProblemSpec:
+    name = name.lower()
+    if d is None:
+        d = default_dimension(name, m)
+    return ProblemSpec(name, d, m)
+
+
+def evaluate_device(spec: ProblemSpec, Xd, out=None):
+    """Enqueue evaluation of a CUDA (n, d) float64 tensor; returns (n, m) tensor."""
+    t = _lib.torch()
+    n = Xd.shape[0]
+    F = out if out is not None else t.empty((n, spec.m), dtype=t.float64, device=Xd.device)
+    rc = _lib.lib().temo_evaluate(_lib.sptr(spec.struct()), _lib.ptr(Xd), n, _lib.ptr(F),
+                                  _lib.stream_handle(Xd.device))
+    _lib.check(rc, "evaluate")
+    return F
+
+
+def evaluate(spec: ProblemSpec, X):
+    """Batch-evaluate n x d decision rows to n x m objectives (problems.py:105-136)."""
+    t = _lib.torch()
+    is_np = not isinstance(X, t.Tensor)
+    A = np.asarray(X, dtype=np.float64) if is_np else X
+    if A.ndim != 2 or A.shape[1] != spec.d:
+        raise ValueError(f"expected n x {spec.d} input, got {tuple(A.shape)}")
+    Xd, _ = _lib.as_device(A, t.float64)
+    F = evaluate_device(spec, Xd)
+    return F.cpu().numpy() if is_np else F
+
+
+def true_front(spec: ProblemSpec, count: int) -> np.ndarray:
+    """Analytic Pareto-front sample for IGD (problems.py:151-184; setup-time host data)."""
+    if count < spec.m:
+        raise ValueError("count must be at least m")
+    m = spec.m
+    if spec.name in ("dtlz1",):
+        return 0.5 * simplex_lattice(m, largest_h_for(count, m))
+    if spec.name in LSMOP:
+        return simplex_lattice(m, largest_h_for(count, m))
+    if spec.name in ("dtlz2", "dtlz3", "dtlz4"):
+        pts = simplex_lattice(m, largest_h_for(count, m))
+        return pts / np.linalg.norm(pts, axis=1, keepdims=True)
+    if spec.name in ("dtlz5", "dtlz6"):
+        theta = np.full((count, m - 1), math.pi / 4.0)
+        theta[:, 0] = np.linspace(0.0, math.pi / 2.0, count)
+        out = np.empty((count, m))
+        for i in range(m):
+            p = np.prod(np.cos(theta[:, : m - 1 - i]), axis=1)
+            if i:
+                p = p * np.sin(theta[:, m - 1 - i])
+            out[:, i] = p
+        return out
+    raise ValueError(f"true_front not provided for {spec.name}")

@@ -1,0 +1,139 @@
+"""GPU parity: device Philox stream, SBX/PM, DTLZ/LSMOP evaluation, fused offspring kernel."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import problems as oprob
+from oracle import variation as ovar
+
+pytestmark = pytest.mark.gpu
+
+
+def philox_gen(seed):
+    return np.random.Generator(np.random.Philox(np.random.SeedSequence(seed)))
+
+
+class ForcedRng:
+    """The reference tests' ForcedRng (oracles.py:108-121)."""
+
+    def __init__(self, value=0.5):
+        self.value = value
+
+    def random(self, size=None):
+        return self.value if size is None else np.full(size, self.value)
+
+    def integers(self, low, high=None, size=None):
+        lo = 0 if high is None else low
+        return np.full(size, lo, dtype=np.int64) if size is not None else lo
+
+
+@pytest.mark.parametrize("pre", [0, 1, 2, 3, 5, 17])
+def test_uniform_stream_bit_exact(cuda, pre):
+    from paper_2503_20286_b200.variation import uniform_device
+
+    a, b = philox_gen(9), philox_gen(9)
+    a.random(pre)
+    b.random(pre)
+    got = uniform_device(a, (1001, 3)).cpu().numpy()
+    assert np.array_equal(got, b.random((1001, 3)))
+    assert np.array_equal(a.permutation(77), b.permutation(77))  # host stream continues identically
+
+
+def test_sbx_pm_golden(cuda):
+    from paper_2503_20286_b200.variation import VariationParams, pair_parents, polynomial_mutation, sbx
+
+    z = load_golden("variation")
+    d = 12
+    rng = philox_gen(int(z["seed"]))
+    i1, i2 = pair_parents(rng, 101)
+    assert np.array_equal(i1, z["i1"]) and np.array_equal(i2, z["i2"])
+    p = VariationParams(lower=np.zeros(d), upper=np.ones(d))
+    kids = sbx(rng, z["X"][i1], z["X"][i2], p)
+    # pow differs from NumPy's in the last ulp for a few inputs
+    assert np.allclose(kids, z["kids"], rtol=1e-13, atol=1e-15)
+    assert np.mean(kids == z["kids"]) > 0.9
+    mut = polynomial_mutation(rng, z["kids"], p)
+    assert np.allclose(mut, z["mut"], rtol=1e-13, atol=1e-15)
+    rng = philox_gen(int(z["seed2"]))
+    p2 = VariationParams(lower=np.full(6, -2.0), upper=np.full(6, 3.0), eta_c=5.0, eta_m=7.0, p_m=0.5,
+                         gene_swap=False)
+    kids2 = sbx(rng, z["X2"][:20], z["X2"][20:], p2)
+    assert np.allclose(kids2, z["kids2"], rtol=1e-13, atol=1e-15)
+    assert np.allclose(polynomial_mutation(rng, z["kids2"], p2), z["mut2"], rtol=1e-13, atol=1e-15)
+
+
+def test_forced_rng_identities(cuda):
+    """test_variation.py:49-145 identities through the injected-draw path."""
+    from paper_2503_20286_b200.variation import VariationParams, polynomial_mutation, sbx
+
+    p = VariationParams(lower=np.zeros(4), upper=np.ones(4))
+    rng = np.random.default_rng(45)
+    X1, X2 = rng.random((5, 4)), rng.random((5, 4))
+    out = sbx(ForcedRng(0.5), X1, X2, p)
+    assert np.array_equal(out[:5], X1) and np.array_equal(out[5:], X2)
+    X = rng.random((6, 4))
+    assert np.array_equal(polynomial_mutation(ForcedRng(0.5), X, p), X)
+    p1 = VariationParams(lower=np.zeros(4), upper=np.ones(4), p_m=1.0)
+    Z = np.zeros((4, 4))
+    assert np.array_equal(polynomial_mutation(ForcedRng(0.3), Z, p1), Z)
+    # identical parents are a fixed point; bounds respected; child-sum identity
+    g = philox_gen(47)
+    same = sbx(g, X, X.copy(), p)
+    assert np.array_equal(same[:6], X) and np.array_equal(same[6:], X)
+    wide = VariationParams(lower=np.full(4, -100.0), upper=np.full(4, 100.0))
+    A, B = rng.random((20, 4)), rng.random((20, 4))
+    c = sbx(philox_gen(46), A, B, wide)
+    assert np.allclose(c[:20] + c[20:], A + B, rtol=0, atol=1e-12)
+
+
+def test_evaluate_golden(cuda):
+    from paper_2503_20286_b200.problems import evaluate, make_problem
+
+    z = load_golden("problems")
+    for key in z.files:
+        if not key.endswith("_X"):
+            continue
+        name, mm = key.split("_")[:2]
+        m = int(mm[1:])
+        spec = make_problem(name, m=m)
+        F = evaluate(spec, z[key])
+        want = z[key[:-1] + "F"]
+        assert np.allclose(F, want, rtol=1e-12, atol=1e-12), key  # north star: 1e-5 rel
+
+
+@pytest.mark.parametrize("m,d", [(3, 1000), (2, 300), (5, 700)])
+def test_lsmop1_vs_self_oracle(cuda, m, d):
+    from paper_2503_20286_b200.problems import evaluate, make_problem
+
+    spec = make_problem("lsmop1", m=m, d=d)
+    rng = np.random.default_rng(d)
+    X = spec.lower + rng.random((200, d)) * (spec.upper - spec.lower)
+    assert np.allclose(evaluate(spec, X), oprob.evaluate_lsmop1(X, m), rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("name,m,d,n", [("dtlz1", 3, 12, 100), ("lsmop1", 3, 1000, 64), ("dtlz2", 5, 40, 33)])
+def test_fused_offspring_matches_oracle(cuda, name, m, d, n):
+    import torch
+
+    from paper_2503_20286_b200.harness import RunConfig, _Stepper
+    from paper_2503_20286_b200.problems import make_problem
+    from paper_2503_20286_b200.directions import das_dennis
+
+    spec = make_problem(name, m=m, d=d)
+    cfg = RunConfig(algorithm="nsga3", problem=name, objectives=m, dim=d, pop_size=n)
+    st_ = _Stepper(cfg, spec, das_dennis(m, 4), n)
+    g_dev, g_ref = philox_gen(3), philox_gen(3)
+    state = st_.init(g_dev)
+    X0 = g_ref.random((n, d))
+    X0 = spec.lower + X0 * (spec.upper - spec.lower)
+    assert np.array_equal(state.X.cpu().numpy(), X0)
+    st_._offspring(state, g_dev)
+    torch.cuda.synchronize()
+    O_ref = ovar.offspring(g_ref, X0, 20.0, 20.0, None, spec.lower, spec.upper)
+    h = n // 2
+    O = state.cur.X[n:n + 2 * h].cpu().numpy()
+    assert np.allclose(O, O_ref, rtol=1e-13, atol=1e-13)
+    FO = state.cur.F[n:n + 2 * h].cpu().numpy()
+    assert np.allclose(FO, oprob.evaluate(name, O_ref, m), rtol=1e-10, atol=1e-12)
+    assert np.array_equal(g_dev.permutation(50), g_ref.permutation(50))
