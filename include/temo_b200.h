@@ -80,14 +80,17 @@ int temo_dominance(const double *F, int64_t N, int m, uint32_t *D_out, int32_t *
  * update_rank, keep) on already-shuffled objectives Fs (N x m) whose ranks
  * come from temo_rank(..., TEMO_RANK_SELECT) (`rank` is updated in place to
  * the final ranks; `l` is the device scalar from temo_rank).
- *   W (nr x m) directions; keep (n int32) receives flatnonzero(rank < l).
+ *   W (nr x m) directions; lattice_H > 0 asserts W == das_dennis(m, H) in its
+ *   row order (directions.py:64-87) and enables the exact O(1)-per-row lattice
+ *   association; 0 = arbitrary direction set (filtered full scan).
+ *   keep (n int32) receives flatnonzero(rank < l).
  *   pi, dist (N) association (nsga3.py:96-116; excluded rows pi=0, dist=NaN);
  *   icpt (m), promoted (<= nr, direction order) always written;
  *   Fp (N x m), ideal (m), extreme (m int64), rho/rho_l (nr), counts (8 int32:
  *   n_promoted, n_s, n_dif, -, kept) optional (NULL to skip). */
 size_t temo_nsga3_select_ws_bytes(int64_t N, int m, int64_t nr);
-int temo_nsga3_select(const double *Fs, int64_t N, int m, const double *W, int64_t nr, int64_t n,
-                      int32_t *rank, const int32_t *l, int32_t *keep, int32_t *pi, double *dist,
+int temo_nsga3_select(const double *Fs, int64_t N, int m, const double *W, int64_t nr,
+                      int32_t lattice_H, int64_t n, int32_t *rank, const int32_t *l, int32_t *keep, int32_t *pi, double *dist,
                       double *Fp, double *ideal, double *icpt, int64_t *extreme, int32_t *rho,
                       int32_t *rho_l, int32_t *promoted, int32_t *counts, int32_t *status, void *ws,
                       size_t ws_bytes, temo_stream_t stream);
@@ -101,8 +104,8 @@ int temo_nsga3_select(const double *Fs, int64_t N, int m, const double *W, int64
  * All share the workspace size temo_nsga3_select_ws_bytes(N, m, nr). */
 int temo_nsga3_normalize(const double *F, int64_t N, int m, double *Fp, double *ideal, double *icpt,
                          int64_t *extreme, void *ws, size_t ws_bytes, temo_stream_t stream);
-int temo_associate(const double *Fp, int64_t N, int m, const double *W, int64_t nr, int32_t *pi,
-                   double *dist, void *ws, size_t ws_bytes, temo_stream_t stream);
+int temo_associate(const double *Fp, int64_t N, int m, const double *W, int64_t nr,
+                   int32_t lattice_H, int32_t *pi, double *dist, void *ws, size_t ws_bytes, temo_stream_t stream);
 int temo_niche_counts(const int32_t *rank, const int32_t *pi, int64_t N, int32_t l, int64_t nr,
                       int32_t *rho, int32_t *rho_l, void *ws, size_t ws_bytes, temo_stream_t stream);
 int temo_niche_select(int32_t *rank, const int32_t *pi, const double *dist, int64_t N, int32_t l,

@@ -37,10 +37,10 @@ SIGNATURES = {
     "temo_dominance_ws_bytes": (_SZ, [_I64, _I32]),
     "temo_dominance": (_I32, [_P, _I64, _I32, _P, _P, _P, _SZ, _P]),
     "temo_nsga3_select_ws_bytes": (_SZ, [_I64, _I32, _I64]),
-    "temo_nsga3_select": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P,
+    "temo_nsga3_select": (_I32, [_P, _I64, _I32, _P, _I64, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P,
                                  _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "temo_nsga3_normalize": (_I32, [_P, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
-    "temo_associate": (_I32, [_P, _I64, _I32, _P, _I64, _P, _P, _P, _SZ, _P]),
+    "temo_associate": (_I32, [_P, _I64, _I32, _P, _I64, _I32, _P, _P, _P, _SZ, _P]),
     "temo_niche_counts": (_I32, [_P, _P, _I64, _I32, _I64, _P, _P, _P, _SZ, _P]),
     "temo_niche_select": (_I32, [_P, _P, _P, _I64, _I32, _P, _I64, _P, _P, _P, _SZ, _P]),
     "temo_update_rank": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _SZ, _P]),

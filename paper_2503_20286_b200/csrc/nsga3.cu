@@ -414,6 +414,158 @@ __global__ void __launch_bounds__(NT) k_associate(const double *__restrict__ F, 
     }
 }
 
+// ---------------------------------------------------------------- lattice association
+// W = das_dennis(m, H): row j is the composition a (sum H) whose cut positions
+// c_k = a_0 + ... + a_k + k enumerate itertools.combinations(range(H+m-1), m-1)
+// in lexicographic order (directions.py:64-82).  For a row f >= 0 the best
+// directions lie within a provable angle of f, so only the lattice points in a
+// small box around the simplex projection p = f / sum(f) are candidates:
+//   - chord <= arc and the projection P(v) = v / sum(v) is (1 + sqrt(m))-Lipschitz
+//     on the positive-orthant unit sphere (sum(v) >= 1 there), so any direction
+//     within angle theta of f has |P(w) - p|_inf <= (1 + sqrt(m)) theta;
+//   - theta* = angle to the nearest-lattice candidate + 1e-6 rad covers the
+//     reference's rounding plateau (|dD| <= ~1e-8 |f| near t = 1 - c^2 = 0).
+// Every candidate in the box is evaluated with the exact reference expression
+// and the (D, index) minimum wins -- identical to the argmin over all rows.
+__device__ __forceinline__ int64_t binom64(int64_t n, int k) {
+    if (k < 0 || n < k) return 0;
+    int64_t r = 1;
+    for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+    return r;
+}
+
+template <int M>
+__device__ __forceinline__ int64_t lattice_index(const int *a, int H) {
+    const int np = H + M - 1, r = M - 1;
+    int64_t rank = 0;
+    int prev = -1;
+    for (int k = 0; k < r; ++k) {
+        const int c = prev + 1 + a[k];
+        const int t = r - 1 - k;
+        rank += binom64(np - prev - 1, t + 1) - binom64(np - c, t + 1);
+        prev = c;
+    }
+    return rank;
+}
+
+constexpr int LATTICE_MAX_BOX = 20000;  // beyond this a row falls back to the full scan
+
+template <int M>
+__global__ void __launch_bounds__(128) k_associate_lattice(
+    const double *__restrict__ F, int64_t N, const int32_t *__restrict__ rank,
+    const int32_t *__restrict__ lp, const double *__restrict__ ideal, const double *__restrict__ icpt,
+    const double *__restrict__ W, const double *__restrict__ U, const double *__restrict__ nw,
+    int64_t nr, int H, int32_t *__restrict__ pi_out, double *__restrict__ dist_out,
+    double *__restrict__ Fp_out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int l = *lp;
+    const double qnan = __longlong_as_double(0x7FF8000000000000ll);
+    if (rank[i] > l) {
+        if (Fp_out)
+            for (int k = 0; k < M; ++k) Fp_out[i * M + k] = qnan;
+        pi_out[i] = 0;
+        dist_out[i] = qnan;
+        return;
+    }
+    double f[M], sq[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        f[k] = (F[i * M + k] - ideal[k]) / icpt[k];
+        sq[k] = f[k] * f[k];
+        if (Fp_out) Fp_out[i * M + k] = f[k];
+    }
+    const double nf = sqrt(np_sum<M>(sq, M));
+    if (!(nf > 0.0) || !isfinite(nf)) {
+        pi_out[i] = 0;
+        dist_out[i] = nf == 0.0 ? 0.0 : qnan;
+        return;
+    }
+    bool nonneg = true;
+    double S = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        nonneg &= f[k] >= 0.0;
+        S += f[k];
+    }
+    double best_d = TEMO_BIG;
+    int64_t best = 0;
+    bool done = false;
+    if (nonneg && S > 0.0) {
+        double p[M];
+        int a[M];
+        // nearest lattice point by largest remainder
+        int tot = 0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            p[k] = f[k] / S;
+            a[k] = (int)floor(p[k] * H);
+            a[k] = a[k] < 0 ? 0 : (a[k] > H ? H : a[k]);
+            tot += a[k];
+        }
+        for (int rem = H - tot; rem > 0; --rem) {
+            int bk = 0;
+            double bfrac = -1.0;
+            for (int k = 0; k < M; ++k) {
+                const double fr = p[k] * H - a[k];
+                if (a[k] < H && fr > bfrac) { bfrac = fr; bk = k; }
+            }
+            a[bk] += 1;
+        }
+        const int64_t j0 = lattice_index<M>(a, H);
+        double s0 = f[0] * U[j0 * M];
+#pragma unroll
+        for (int k = 1; k < M; ++k) s0 = fma(f[k], U[j0 * M + k], s0);
+        double c0 = s0 / nf;
+        c0 = c0 > 1.0 ? 1.0 : (c0 < -1.0 ? -1.0 : c0);
+        const double theta = acos(c0) + 1e-6;
+        const double R = (1.0 + sqrt((double)M)) * theta;
+        int lo[M], hi[M];
+        double vol = 1.0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            const double lf = floor((p[k] - R) * H), hf = ceil((p[k] + R) * H);
+            lo[k] = lf < 0.0 ? 0 : (lf > H ? H : (int)lf);
+            hi[k] = hf > H ? H : (hf < 0.0 ? 0 : (int)hf);
+            if (k < M - 1) vol *= (double)(hi[k] - lo[k] + 1);
+        }
+        if (vol <= LATTICE_MAX_BOX) {
+            done = true;
+            // odometer over a_0..a_{M-2}; a_{M-1} = H - sum, must lie in [lo, hi]
+            int c[M];
+            for (int k = 0; k < M - 1; ++k) c[k] = lo[k];
+            while (true) {
+                int sum = 0;
+                for (int k = 0; k < M - 1; ++k) sum += c[k];
+                const int last = H - sum;
+                if (last >= lo[M - 1] && last <= hi[M - 1]) {
+                    c[M - 1] = last;
+                    const int64_t j = lattice_index<M>(c, H);
+                    const double d = exact_D(f, W + j * M, M, nf, nw[j]);
+                    if (d < best_d || (d == best_d && j < best)) { best_d = d; best = j; }
+                }
+                int k = M - 2;
+                while (k >= 0) {
+                    if (++c[k] <= hi[k]) break;
+                    c[k] = lo[k];
+                    --k;
+                }
+                if (k < 0) break;
+            }
+        }
+    }
+    if (!done) {  // general position: exact scan of every direction
+        best_d = TEMO_BIG;
+        best = 0;
+        for (int64_t j = 0; j < nr; ++j) {
+            const double d = exact_D(f, W + j * M, M, nf, nw[j]);
+            if (d < best_d || j == 0) { best_d = d; best = j; }
+        }
+    }
+    pi_out[i] = (int32_t)best;
+    dist_out[i] = best_d;
+}
+
 // ---------------------------------------------------------------- niching
 __global__ void k_niche_count(const int32_t *__restrict__ rank, const int32_t *__restrict__ pi,
                               const int32_t *__restrict__ lp, int64_t N, int32_t *__restrict__ rho,
@@ -621,13 +773,29 @@ static int stage_normalize(SelPlan &p, const double *F, const int32_t *rank, con
     return TEMO_OK;
 }
 
-// nsga3.py:96-116 on (F - ideal)/icpt for rows with rank <= *l
+// nsga3.py:96-116 on (F - ideal)/icpt for rows with rank <= *l.  lattice_H > 0
+// asserts W == das_dennis(m, H) in its row order: exact lattice search.
 static int stage_associate(SelPlan &p, const double *F, const int32_t *rank, const int32_t *l,
                            const double *ideal, const double *icpt, const double *W, int32_t *pi,
-                           double *dist, double *Fp, cudaStream_t st) {
+                           double *dist, double *Fp, int lattice_H, cudaStream_t st) {
     const int64_t N = p.N, nr = p.nr;
     const int m = p.m;
     k_dir_prep<<<g1(nr), NT, 0, st>>>(W, nr, m, p.nw, p.U);
+    if (lattice_H > 0 && m >= 2) {
+#define ASSOCL(MM)                                                                                  \
+    case MM:                                                                                        \
+        k_associate_lattice<MM><<<g1(N, 128), 128, 0, st>>>(F, N, rank, l, ideal, icpt, W, p.U,    \
+                                                             p.nw, nr, lattice_H, pi, dist, Fp);  \
+        break;
+        switch (m) {
+            ASSOCL(2) ASSOCL(3) ASSOCL(4) ASSOCL(5) ASSOCL(6) ASSOCL(7) ASSOCL(8) ASSOCL(9)
+            ASSOCL(10) ASSOCL(11) ASSOCL(12) ASSOCL(13) ASSOCL(14) ASSOCL(15) ASSOCL(16)
+            default: return TEMO_EINVAL;
+        }
+#undef ASSOCL
+        TEMO_LAUNCH_CHECK();
+        return TEMO_OK;
+    }
 #define ASSOC(MM)                                                                                  \
     case MM:                                                                                       \
         k_associate<MM><<<g1(N), NT, 0, st>>>(F, N, rank, l, ideal, icpt, W, p.U, p.nw, nr, pi, \
@@ -716,7 +884,7 @@ extern "C" size_t temo_nsga3_select_ws_bytes(int64_t N, int m, int64_t nr) {
 }
 
 extern "C" int temo_nsga3_select(const double *Fs, int64_t N, int m, const double *W, int64_t nr,
-                                 int64_t n, int32_t *rank, const int32_t *l, int32_t *keep,
+                                 int32_t lattice_H, int64_t n, int32_t *rank, const int32_t *l, int32_t *keep,
                                  int32_t *pi, double *dist, double *Fp, double *ideal_out,
                                  double *icpt, int64_t *extreme, int32_t *rho_out,
                                  int32_t *rho_l_out, int32_t *promoted, int32_t *counts,
@@ -732,7 +900,7 @@ extern "C" int temo_nsga3_select(const double *Fs, int64_t N, int m, const doubl
     if ((rc = stage_normalize(p, Fs, rank, l, ideal, icpt, extreme, st))) return rc;
     stage_end(S_NORMALIZE, st);
     stage_begin(S_ASSOCIATE, st);
-    if ((rc = stage_associate(p, Fs, rank, l, ideal, icpt, W, pi, dist, Fp, st))) return rc;
+    if ((rc = stage_associate(p, Fs, rank, l, ideal, icpt, W, pi, dist, Fp, lattice_H, st))) return rc;
     stage_end(S_ASSOCIATE, st);
     stage_begin(S_NICHE, st);
     if ((rc = stage_counts(p, rank, pi, l, rho, rho_l_out, st))) return rc;
@@ -764,7 +932,7 @@ extern "C" int temo_nsga3_normalize(const double *F, int64_t N, int m, double *F
 
 // nsga3.associate(Fp, R) (nsga3.py:96-116) on a given Fp (rows with NaN -> pi 0, dist NaN)
 extern "C" int temo_associate(const double *Fp, int64_t N, int m, const double *W, int64_t nr,
-                              int32_t *pi, double *dist, void *ws, size_t ws_bytes,
+                              int32_t lattice_H, int32_t *pi, double *dist, void *ws, size_t ws_bytes,
                               temo_stream_t stream) {
     if (N < 1 || m < 1 || m > MAXM || nr < 1 || !Fp || !W || !pi || !dist) return TEMO_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
@@ -773,7 +941,7 @@ extern "C" int temo_associate(const double *Fp, int64_t N, int m, const double *
     k_set_scalar<<<1, 1, 0, st>>>(p.lbuf, 0);
     TEMO_CUDA(cudaMemsetAsync(p.zero, 0, sizeof(double) * MAXM, st));
     k_fill_u64<<<1, MAXM, 0, st>>>((unsigned long long *)p.one, MAXM, 0x3FF0000000000000ull);
-    return stage_associate(p, Fp, p.rankbuf, p.lbuf, p.zero, p.one, W, pi, dist, nullptr, st);
+    return stage_associate(p, Fp, p.rankbuf, p.lbuf, p.zero, p.one, W, pi, dist, nullptr, lattice_H, st);
 }
 
 // nsga3.niche_counts (nsga3.py:119-123); l is a host value

@@ -80,8 +80,11 @@ def normalize(F) -> NormalizedObjectives:
     return NormalizedObjectives(_out(Fp, was_np), _out(ideal, was_np), _out(icpt, was_np))
 
 
-def associate(Fp, R: DirectionSet) -> AssociationResult:
-    """Perpendicular-nearest direction, first index on ties (nsga3.py:96-116)."""
+def associate(Fp, R: DirectionSet, lattice: bool = True) -> AssociationResult:
+    """Perpendicular-nearest direction, first index on ties (nsga3.py:96-116).
+
+    For das_dennis direction sets the exact lattice search is used (``lattice``
+    False forces the filtered full scan; both are bit-identical)."""
     t = _t()
     Fd, was_np = _lib.as_device(Fp, t.float64)
     N, m = Fd.shape
@@ -89,7 +92,8 @@ def associate(Fp, R: DirectionSet) -> AssociationResult:
     pi = t.empty(N, dtype=t.int32, device=Fd.device)
     dist = t.empty(N, dtype=t.float64, device=Fd.device)
     ws = _ws(N, m, R.count, Fd.device)
-    rc = _lib.lib().temo_associate(_lib.ptr(Fd), N, m, _lib.ptr(Wd), R.count, _lib.ptr(pi),
+    rc = _lib.lib().temo_associate(_lib.ptr(Fd), N, m, _lib.ptr(Wd), R.count,
+                                   R.lattice_H if lattice else 0, _lib.ptr(pi),
                                    _lib.ptr(dist), _lib.ptr(ws), ws.numel(), _lib.stream_handle(Fd.device))
     _lib.check(rc, "associate")
     return AssociationResult(_out(pi.to(t.int64), was_np), _out(dist, was_np))
@@ -160,8 +164,9 @@ class Nsga3Selector:
     indices into the shuffled order (ascending), like ``flatnonzero(rank < l)``.
     """
 
-    def __init__(self, N: int, m: int, R: DirectionSet, n: int, dev=None, record=False):
+    def __init__(self, N: int, m: int, R: DirectionSet, n: int, dev=None, record=False, lattice=True):
         t = _t()
+        self.lattice_H = R.lattice_H if lattice else 0
         self.dev = _lib.device(dev)
         self.N, self.m, self.n = N, m, n
         self.R = R
@@ -196,7 +201,8 @@ class Nsga3Selector:
         L = _lib.lib()
         ws = _lib.workspace.get(self.ws_sel, self.dev)
         p = _lib.ptr
-        rc = L.temo_nsga3_select(p(self.Fs), self.N, self.m, p(self.W), self.R.count, self.n, p(self.rank),
+        rc = L.temo_nsga3_select(p(self.Fs), self.N, self.m, p(self.W), self.R.count, self.lattice_H,
+                                 self.n, p(self.rank),
                                  p(self.l), p(self.keep), p(self.pi), p(self.dist), p(self.Fp),
                                  p(self.ideal), p(self.icpt), p(self.extreme), p(self.rho), p(self.rho_l),
                                  p(self.promoted), p(self.counts), p(self.status), p(ws), ws.numel(),

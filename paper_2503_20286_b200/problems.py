@@ -122,7 +122,8 @@ def evaluate_device(spec: ProblemSpec, Xd, out=None):
     t = _lib.torch()
     n = Xd.shape[0]
     F = out if out is not None else t.empty((n, spec.m), dtype=t.float64, device=Xd.device)
-    rc = _lib.lib().temo_evaluate(_lib.sptr(spec.struct()), _lib.ptr(Xd), n, _lib.ptr(F),
+    ps = spec.struct()  # keep the struct alive across the call
+    rc = _lib.lib().temo_evaluate(_lib.sptr(ps), _lib.ptr(Xd), n, _lib.ptr(F),
                                   _lib.stream_handle(Xd.device))
     _lib.check(rc, "evaluate")
     return F

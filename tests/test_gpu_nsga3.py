@@ -184,6 +184,40 @@ def test_selection_vs_oracle_random(cuda, N, m, H, seed):
     assert np.array_equal(keep, want["keep"])
 
 
+@pytest.mark.parametrize("m,H,N", [(3, 630, 60000), (3, 76, 20000), (2, 300, 5000), (4, 12, 8000),
+                                   (5, 8, 4000), (3, 7, 3000)])
+def test_lattice_association_equals_full_scan(cuda, m, H, N):
+    """The O(1)-per-row lattice search is bit-identical to the argmin over all directions."""
+    from paper_2503_20286_b200.directions import das_dennis
+    from paper_2503_20286_b200.nsga3 import associate
+
+    R = das_dennis(m, H)
+    assert R.lattice_H == H
+    rng = np.random.default_rng(H + m)
+    Fp = rng.random((N, m)) ** 3
+    Fp[: N // 10] = np.round(Fp[: N // 10] * H) / H  # rows exactly on lattice directions
+    Fp[N // 10: N // 5, 0] = 0.0                         # rows on a face
+    Fp[5] = 0.0
+    a = associate(Fp, R, lattice=True)
+    b = associate(Fp, R, lattice=False)
+    assert np.array_equal(a.pi, b.pi)
+    assert np.array_equal(a.dist, b.dist)
+    sub = rng.choice(N, 300, replace=False)
+    pi, dist = onsga3.associate(Fp[sub], R.W)
+    assert np.array_equal(a.pi[sub], pi) and np.array_equal(a.dist[sub], dist)
+
+
+def test_lattice_index_order(cuda):
+    """Lattice-index decoding agrees with das_dennis row order (checked through associate)."""
+    from paper_2503_20286_b200.directions import das_dennis
+    from paper_2503_20286_b200.nsga3 import associate
+
+    for m, H in ((3, 9), (4, 5), (6, 3)):
+        R = das_dennis(m, H)
+        a = associate(R.W * 2.0, R)  # every direction is its own nearest
+        assert np.array_equal(a.pi, np.arange(R.count))
+
+
 def test_neighbors_golden(cuda):
     from paper_2503_20286_b200.directions import DirectionSet, neighbors
 
