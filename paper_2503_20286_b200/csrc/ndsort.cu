@@ -203,79 +203,119 @@ __device__ __forceinline__ int64_t items_before(int64_t T) {
     return T + CHUNK * a * (a - 1) / 2 + r * a;
 }
 
+// 32x32 bit transpose across a warp: lane r holds row r (bit c = element (r, c));
+// returns, in lane c, the column c (bit r = element (r, c)).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const uint32_t lowmask = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
+                                                                : s == 2 ? 0x33333333u : 0x55555555u;
+        const bool top = (lane & s) == 0;
+        const uint32_t keep = top ? lowmask : ~lowmask;
+        const uint32_t y = __shfl_xor_sync(~0u, x, s) & keep;
+        x = (x & keep) | (top ? (y << s) : (y >> s));
+    }
+    return x;
+}
+
+// K1: lane owns row i (sorted order) and walks the columns j of a 256-wide
+// tile broadcast from shared memory.  With d_k = r_k(j) - r_k(i) (two's
+// complement, ranks < 2^20) row i dominates j iff no d_k is negative, so one
+// OR of the differences puts "not dominated" in the sign bit and a funnel
+// shift collects 32 of them into a register word: per (lane, column) two
+// integer adds (FMA pipe), one LOP3 and one SHF (ALU pipe), no ballot, no
+// per-pair shared-memory store.  Each finished word is also transposed
+// across the warp and popcounted, which yields the dominated-by counts of the
+// 32 columns among the warp's 32 rows (the peel's initial counts).
 template <int M>
-__global__ void __launch_bounds__(TILE) k_dom_bits(const uint4 *__restrict__ rec, int64_t N,
+__global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec, int64_t N,
                                                    int64_t nT, int64_t W,
                                                    const int64_t *__restrict__ rt_off,
-                                                   uint32_t *__restrict__ bits) {
+                                                   uint32_t *__restrict__ bits,
+                                                   int32_t *__restrict__ cnt) {
     constexpr int NV = (M + 3) / 4;
-    __shared__ uint4 sI[TILE * NV];
-    __shared__ __align__(16) uint32_t sB[TILE * 8];
-    __shared__ int64_t s_jt, s_chunk;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    __shared__ uint4 sJ[TILE * NV];
+    __shared__ uint32_t sB[TILE * 9];  // row-major [i][jw], stride 9: conflict-free
+    __shared__ int32_t sCnt[TILE];
+    __shared__ int64_t s_it, s_chunk;
+    const int tid = threadIdx.x, lane = tid & 31;
     if (tid == 0) {
+        // strip t = nT-1-I owns t+1 column tiles -> floor(t/CHUNK)+1 items
         int64_t item = blockIdx.x, lo = 0, hi = nT - 1;
         while (lo < hi) {
             int64_t mid = (lo + hi + 1) >> 1;
             if (items_before(mid) <= item) lo = mid; else hi = mid - 1;
         }
-        s_jt = lo;
+        s_it = nT - 1 - lo;
         s_chunk = item - items_before(lo);
     }
     __syncthreads();
-    const int64_t jt = s_jt, chunk = s_chunk;
-    const int64_t j = jt * TILE + tid;
-    uint4 rj[NV];
+    const int64_t it = s_it, chunk = s_chunk;
+    const int64_t i = it * TILE + tid;
+    // own row: negated fields so that v + n = r(j) - r(i); id field: id(j) - id(i) - 1
+    uint32_t nf[4 * NV];
+    {
+        uint4 ri[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) rj[v] = rec[j * NV + v];
-    const uint32_t jmin_id = fld(&rec[jt * TILE * NV], M - 1);
-    const int64_t it0 = chunk * CHUNK;
-    const int64_t it1 = min(it0 + CHUNK, jt + 1);
-    for (int64_t it = it0; it < it1; ++it) {
+        for (int v = 0; v < NV; ++v) ri[v] = rec[i * NV + v];
+#pragma unroll
+        for (int k = 0; k < 4 * NV; ++k) nf[k] = 0u - fld(ri, k);
+        nf[M - 1] -= 1u;
+    }
+    const bool row_ok = i < N;
+    const uint32_t last_i_id = fld(&rec[(it * TILE + TILE - 1) * NV], M - 1);
+    const int64_t jt0 = it + chunk * CHUNK;
+    const int64_t jt1 = min(jt0 + CHUNK, nT);
+    for (int64_t jt = jt0; jt < jt1; ++jt) {
         __syncthreads();
 #pragma unroll
-        for (int v = 0; v < NV; ++v) sI[tid * NV + v] = rec[(it * TILE + tid) * NV + v];
+        for (int v = 0; v < NV; ++v) sJ[tid * NV + v] = rec[(jt * TILE + tid) * NV + v];
+        sCnt[tid] = 0;
         __syncthreads();
-        const bool disjoint = fld(&sI[(TILE - 1) * NV], M - 1) < jmin_id;
-        if (disjoint) {
+        // ids of the two tiles do not overlap -> the id test is implied (and M == 1 needs it)
+        const bool disjoint = M > 1 && last_i_id < fld(&sJ[0], M - 1);
+#pragma unroll 1
+        for (int jw = 0; jw < 8; ++jw) {
+            uint32_t acc = 0;
+            if (disjoint) {
 #pragma unroll 8
-            for (int i = 0; i < TILE; ++i) {
-                bool P = true;
+                for (int b = 0; b < 32; ++b) {
+                    const uint4 *v = &sJ[(jw * 32 + b) * NV];
+                    uint32_t x = 0;
 #pragma unroll
-                for (int k = 0; k < M - 1; ++k) P &= fld(&sI[i * NV], k) <= fld(rj, k);
-                const uint32_t b = __ballot_sync(~0u, P);
-                if (lane == 0) sB[i * 8 + warp] = b;
-            }
-        } else {
-#pragma unroll 4
-            for (int i = 0; i < TILE; ++i) {
-                bool P = fld(&sI[i * NV], M - 1) < fld(rj, M - 1);
+                    for (int k = 0; k < M - 1; ++k) x |= fld(v, k) + nf[k];
+                    acc = __funnelshift_l(x, acc, 1);
+                }
+            } else {
+#pragma unroll 8
+                for (int b = 0; b < 32; ++b) {
+                    const uint4 *v = &sJ[(jw * 32 + b) * NV];
+                    uint32_t x = fld(v, M - 1) + nf[M - 1];
 #pragma unroll
-                for (int k = 0; k < M - 1; ++k) P &= fld(&sI[i * NV], k) <= fld(rj, k);
-                const uint32_t b = __ballot_sync(~0u, P);
-                if (lane == 0) sB[i * 8 + warp] = b;
+                    for (int k = 0; k < M - 1; ++k) x |= fld(v, k) + nf[k];
+                    acc = __funnelshift_l(x, acc, 1);
+                }
             }
+            // bit 31-b of acc = "j = 32 jw + b not dominated by i"
+            uint32_t word = row_ok ? __brev(~acc) : 0u;
+            if (jt == nT - 1) {  // padding columns past N
+                const int64_t base = jt * TILE + 32 * jw;
+                word &= base + 32 <= N ? ~0u : (base >= N ? 0u : (1u << (N - base)) - 1u);
+            }
+            sB[tid * 9 + jw] = word;
+            const uint32_t col = warp_transpose32(word, lane);
+            const int c = __popc(col);
+            if (c) atomicAdd(&sCnt[jw * 32 + lane], c);
         }
         __syncthreads();
-        const int64_t i = it * TILE + tid;
-        if (i < N) {
+        if (row_ok) {
             uint32_t *dst = bits + rt_off[it] + (int64_t)tid * (W - 8 * it) + 8 * (jt - it);
-            const uint4 *src = reinterpret_cast<const uint4 *>(sB) + tid * 2;
-            uint4 lo = src[0], hi = src[1];
-            if (jt == nT - 1) {  // columns past N carry padding records: mask them
-                uint32_t w8[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int64_t base = jt * TILE + 32 * q;
-                    const uint32_t vm = base + 32 <= N ? ~0u : (base >= N ? 0u : (1u << (N - base)) - 1u);
-                    w8[q] &= vm;
-                }
-                lo = make_uint4(w8[0], w8[1], w8[2], w8[3]);
-                hi = make_uint4(w8[4], w8[5], w8[6], w8[7]);
-            }
-            reinterpret_cast<uint4 *>(dst)[0] = lo;
-            reinterpret_cast<uint4 *>(dst)[1] = hi;
+            const uint32_t *s = sB + tid * 9;
+            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(s[0], s[1], s[2], s[3]);
+            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(s[4], s[5], s[6], s[7]);
         }
+        const int c = sCnt[tid];
+        if (c) atomicAdd(cnt + jt * TILE + tid, c);
     }
 }
 
@@ -344,17 +384,30 @@ __device__ void vertical_pass(const PeelArgs &a, const int *rows_below, const in
         const int r0 = chunk * LC + warp * ROWS_PER_WARP;
         const int r1 = min(r0 + ROWS_PER_WARP, rows_below[wb]);
         const int64_t w = (int64_t)wb * 32 + lane;
+        // lane k resolves row r0+k once (list entry, row base address, first stored
+        // word); the row loop then only shuffles and issues independent loads
+        const int rr = max(r1 - r0, 0);
+        int64_t my_base = 0;
+        int my_w0 = 0x7FFFFFFF;
+        if (lane < rr) {
+            const int i = identity ? r0 + lane : a.list[r0 + lane];
+            const int64_t it = i >> 8;
+            my_base = a.rt_off[it] + (int64_t)(i & 255) * (a.W - 8 * it) - 8 * it;
+            my_w0 = (int)(8 * it);
+        }
         uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0, o0 = 0, o1 = 0, o2 = 0, o3 = 0;
-        for (int g = r0; g < r1; g += 15) {
-            const int ge = min(g + 15, r1);
+        for (int g = 0; g < rr; g += 15) {
+            uint32_t xs[15];
+#pragma unroll
+            for (int q = 0; q < 15; ++q) {
+                const int64_t b = __shfl_sync(~0u, my_base, (g + q) & 31);
+                const int w0 = __shfl_sync(~0u, my_w0, (g + q) & 31);
+                xs[q] = (g + q < rr && w >= w0) ? __ldg(a.bits + b + w) : 0u;
+            }
             uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-#pragma unroll 5
-            for (int r = g; r < ge; ++r) {
-                const int i = identity ? r : a.list[r];
-                const int64_t it = i >> 8;
-                uint32_t x = 0;
-                if (w >= 8 * it)
-                    x = __ldg(a.bits + a.rt_off[it] + (int64_t)(i & 255) * (a.W - 8 * it) + (w - 8 * it));
+#pragma unroll
+            for (int q = 0; q < 15; ++q) {
+                const uint32_t x = xs[q];
                 a0 += x & 0x11111111u;
                 a1 += (x >> 1) & 0x11111111u;
                 a2 += (x >> 2) & 0x11111111u;
@@ -395,17 +448,7 @@ __global__ void __launch_bounds__(PEEL_T) k_peel(PeelArgs a) {
     uint32_t *sred = reinterpret_cast<uint32_t *>(s_tmp + 32);  // 8*8*32
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    // ---- initial dominated-by counts: all rows, identity list, sign +1
-    for (int wb = tid; wb < a.NB; wb += PEEL_T) {
-        const int rb = min(a.N, (wb + 1) * 1024);
-        s_rows[wb] = rb;
-        s_items[wb] = (rb + LC - 1) / LC;
-    }
-    if (tid == 0) s_items[a.NB] = 0;
-    __syncthreads();
-    block_exclusive_scan(s_items, a.NB + 1, s_tmp);
-    vertical_pass(a, s_rows, s_items, true, +1, sred);
-    grid.sync();
+    // initial dominated-by counts come from K1 (column popcounts of each tile)
 
     int ranked = 0, l = -1, k = 0;
     while (true) {
@@ -480,7 +523,7 @@ __global__ void k_peel_init(int32_t *rank_s, int32_t *cnt, int64_t N, int64_t Np
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= Np) return;
     rank_s[p] = p < N ? -1 : 0x7FFFFFFF;
-    cnt[p] = 0;
+    (void)cnt;  // counts were produced by K1
 }
 
 __global__ void k_unsort_ranks(const int32_t *__restrict__ rank_s, const int32_t *__restrict__ order,
@@ -559,8 +602,9 @@ static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStrea
     const int64_t items = p.nT + CHUNK * ((p.nT / CHUNK) * ((p.nT / CHUNK) - 1) / 2) +
                           (p.nT % CHUNK) * (p.nT / CHUNK);
     const dim3 g((unsigned)items);
+    TEMO_CUDA(cudaMemsetAsync(p.cnt, 0, sizeof(int32_t) * p.Np, st));
 #define DOM_CASE(MM) \
-    case MM: k_dom_bits<MM><<<g, TILE, 0, st>>>(p.rec, N, p.nT, p.W, p.rt_off, p.bits); break;
+    case MM: k_dom_rows<MM><<<g, TILE, 0, st>>>(p.rec, N, p.nT, p.W, p.rt_off, p.bits, p.cnt); break;
     switch (m) {
         DOM_CASE(1) DOM_CASE(2) DOM_CASE(3) DOM_CASE(4) DOM_CASE(5) DOM_CASE(6) DOM_CASE(7)
         DOM_CASE(8) DOM_CASE(9) DOM_CASE(10) DOM_CASE(11) DOM_CASE(12) DOM_CASE(13) DOM_CASE(14)
