@@ -204,29 +204,47 @@ __device__ __forceinline__ int64_t items_before(int64_t T) {
 }
 
 // 32x32 bit transpose across a warp: lane r holds row r (bit c = element (r, c));
-// returns, in lane c, the column c (bit r = element (r, c)).
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+// returns, in lane c, the column c (bit r = element (r, c)).  Each butterfly
+// stage is SHFL + one per-lane rotate + one LOP3: the rotate amount (s or 32-s)
+// and the keep mask are lane constants, and wrapped-around bits always land in
+// the masked-off half.
+struct Transpose32 {
+    uint32_t keep[5];
+    uint32_t rot[5];
+    __device__ __forceinline__ explicit Transpose32(int lane) {
 #pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-        const uint32_t lowmask = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu
-                                                                : s == 2 ? 0x33333333u : 0x55555555u;
-        const bool top = (lane & s) == 0;
-        const uint32_t keep = top ? lowmask : ~lowmask;
-        const uint32_t y = __shfl_xor_sync(~0u, x, s) & keep;
-        x = (x & keep) | (top ? (y << s) : (y >> s));
+        for (int q = 0; q < 5; ++q) {
+            const int s = 16 >> q;
+            const uint32_t lowmask = q == 0 ? 0x0000FFFFu : q == 1 ? 0x00FF00FFu : q == 2 ? 0x0F0F0F0Fu
+                                   : q == 3 ? 0x33333333u : 0x55555555u;
+            const bool top = (lane & s) == 0;
+            keep[q] = top ? lowmask : ~lowmask;
+            rot[q] = top ? s : 32 - s;
+        }
     }
-    return x;
-}
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const uint32_t y = __shfl_xor_sync(~0u, x, 16 >> q);
+            const uint32_t t = __funnelshift_l(y, y, rot[q]);  // rotate left
+            x = (x & keep[q]) | (t & ~keep[q]);
+        }
+        return x;
+    }
+};
 
 // K1: lane owns row i (sorted order) and walks the columns j of a 256-wide
 // tile broadcast from shared memory.  With d_k = r_k(j) - r_k(i) (two's
 // complement, ranks < 2^20) row i dominates j iff no d_k is negative, so one
 // OR of the differences puts "not dominated" in the sign bit and a funnel
-// shift collects 32 of them into a register word: per (lane, column) two
-// integer adds (FMA pipe), one LOP3 and one SHF (ALU pipe), no ballot, no
-// per-pair shared-memory store.  Each finished word is also transposed
-// across the warp and popcounted, which yields the dominated-by counts of the
-// 32 columns among the warp's 32 rows (the peel's initial counts).
+// shift collects 32 of them into a register word: per (lane, column) the
+// integer subtractions issue on the FMA pipe (IMAD.IADD) and one LOP3 + one
+// SHF on the ALU pipe -- no ballot, no per-pair shared-memory store.  For
+// m <= 3 the columns' rank fields are packed densely in shared memory so one
+// LDS.128 serves 2 (m = 3) or 4 (m = 2) columns.  Each finished word is also
+// transposed across the warp and popcounted, which yields the dominated-by
+// counts of the 32 columns among the warp's 32 rows (the peel's initial
+// counts; no full-triangle counting pass).
 template <int M>
 __global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec, int64_t N,
                                                    int64_t nT, int64_t W,
@@ -234,7 +252,10 @@ __global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec
                                                    uint32_t *__restrict__ bits,
                                                    int32_t *__restrict__ cnt) {
     constexpr int NV = (M + 3) / 4;
+    constexpr int FD = M - 1;                    // rank fields compared in disjoint tiles
+    constexpr bool PACK = FD == 1 || FD == 2;    // dense packing for m = 2, 3
     __shared__ uint4 sJ[TILE * NV];
+    __shared__ __align__(16) uint32_t sP[PACK ? TILE * FD : 4];
     __shared__ uint32_t sB[TILE * 9];  // row-major [i][jw], stride 9: conflict-free
     __shared__ int32_t sCnt[TILE];
     __shared__ int64_t s_it, s_chunk;
@@ -264,20 +285,45 @@ __global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec
     }
     const bool row_ok = i < N;
     const uint32_t last_i_id = fld(&rec[(it * TILE + TILE - 1) * NV], M - 1);
+    const Transpose32 transpose(lane);
     const int64_t jt0 = it + chunk * CHUNK;
     const int64_t jt1 = min(jt0 + CHUNK, nT);
     for (int64_t jt = jt0; jt < jt1; ++jt) {
         __syncthreads();
+        uint4 rv[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) sJ[tid * NV + v] = rec[(jt * TILE + tid) * NV + v];
+        for (int v = 0; v < NV; ++v) {
+            rv[v] = rec[(jt * TILE + tid) * NV + v];
+            sJ[tid * NV + v] = rv[v];
+        }
+        if (PACK) {
+#pragma unroll
+            for (int k = 0; k < FD; ++k) sP[tid * FD + k] = fld(rv, k);
+        }
         sCnt[tid] = 0;
         __syncthreads();
         // ids of the two tiles do not overlap -> the id test is implied (and M == 1 needs it)
         const bool disjoint = M > 1 && last_i_id < fld(&sJ[0], M - 1);
+        const bool last_tile = jt == nT - 1;
 #pragma unroll 1
         for (int jw = 0; jw < 8; ++jw) {
             uint32_t acc = 0;
-            if (disjoint) {
+            if (disjoint && PACK) {
+                const uint4 *q4 = reinterpret_cast<const uint4 *>(sP) + jw * 32 * FD / 4;
+#pragma unroll
+                for (int c = 0; c < 8 * FD; ++c) {
+                    const uint4 v = q4[c];
+                    if (FD == 2) {
+                        acc = __funnelshift_l((v.x + nf[0]) | (v.y + nf[1]), acc, 1);
+                        acc = __funnelshift_l((v.z + nf[0]) | (v.w + nf[1]), acc, 1);
+                    } else {
+                        acc = __funnelshift_l(v.x + nf[0], acc, 1);
+                        acc = __funnelshift_l(v.y + nf[0], acc, 1);
+                        acc = __funnelshift_l(v.z + nf[0], acc, 1);
+                        acc = __funnelshift_l(v.w + nf[0], acc, 1);
+                    }
+                }
+            } else if (disjoint) {
 #pragma unroll 8
                 for (int b = 0; b < 32; ++b) {
                     const uint4 *v = &sJ[(jw * 32 + b) * NV];
@@ -298,13 +344,12 @@ __global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec
             }
             // bit 31-b of acc = "j = 32 jw + b not dominated by i"
             uint32_t word = row_ok ? __brev(~acc) : 0u;
-            if (jt == nT - 1) {  // padding columns past N
+            if (last_tile) {  // padding columns past N
                 const int64_t base = jt * TILE + 32 * jw;
                 word &= base + 32 <= N ? ~0u : (base >= N ? 0u : (1u << (N - base)) - 1u);
             }
             sB[tid * 9 + jw] = word;
-            const uint32_t col = warp_transpose32(word, lane);
-            const int c = __popc(col);
+            const int c = __popc(transpose(word));
             if (c) atomicAdd(&sCnt[jw * 32 + lane], c);
         }
         __syncthreads();
