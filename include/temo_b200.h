@@ -184,9 +184,60 @@ int temo_offspring(const temo_problem *prob, const temo_variation *var, const do
                    const int64_t *i1, const int64_t *i2, int64_t h, const temo_philox_state *st,
                    uint64_t off, double *O, double *FO, temo_stream_t stream);
 
+/* ------------------------------------------------------------------ MOEA/D
+ * temo_moead_offspring: moead.moead_offspring (moead.py:127-145) for parents
+ *   p1[i], p2[i] (rows of X): SBX child c1 only, PM, evaluate -> O, FO (n rows);
+ *   draws from `off`: SBX mu/swap/crossed then PM mu/hit, n*d each.
+ * temo_moead_compare: moead.compare_update (moead.py:70-92) without the n x n
+ *   matrix: zmin (m), g_new (n x T) and improves (n x T, 0/1).
+ * temo_moead_elite: moead.elite_select (moead.py:95-124) in O(n T) via the
+ *   reverse CSR (rptr n+1, rcol = i*T + t sorted by i) of I_nb; winner (n,
+ *   -1 = incumbent), Xn (n x d), Fn (n x m).
+ * temo_aggregate_rows: moead.pbi (moead.py:43-67) / Tchebycheff on aligned rows.
+ * kind: TEMO_AGG_PBI (reference) or TEMO_AGG_TCH (new; parity unpinned). */
+#define TEMO_AGG_PBI 0
+#define TEMO_AGG_TCH 1
+int temo_moead_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
+                         const int64_t *p1, const int64_t *p2, int64_t n,
+                         const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                         temo_stream_t stream);
+int temo_moead_compare(const double *F1, const double *F2, const double *W, const int32_t *I_nb,
+                       int64_t n, int T, int m, const double *z, double theta, int kind,
+                       double *zmin, double *g_new, uint8_t *improves, temo_stream_t stream);
+int temo_moead_elite(const double *X, const double *F1, const double *W, const double *O,
+                     const double *F2, int64_t n, int64_t d, int T, int m, const double *zmin,
+                     double theta, int kind, const int64_t *rptr, const int32_t *rcol,
+                     const double *g_new, const uint8_t *improves, int32_t *winner, double *Xn,
+                     double *Fn, temo_stream_t stream);
+int temo_aggregate_rows(const double *f, const double *w, const double *z, int64_t rows, int m,
+                        double theta, int kind, int normalize, double *out, temo_stream_t stream);
+
 /* harness._Stepper.init (harness.py:188-190): X = lower + U (upper - lower), U from the stream. */
 int temo_init_population(const temo_philox_state *st, uint64_t off, int64_t rows, int64_t d,
                          const double *lower, const double *upper, double *X, temo_stream_t stream);
+
+/* -------------------------------------------------------------------- HypE
+ * temo_hype_alpha: hype.shared_alpha (hype.py:37-51) -> alpha (n1).
+ * temo_hv_estimate: hype.hv_estimate (hype.py:54-85) with v_ref (device, m)
+ *   and k given; uniforms from the stream at `off` (s*m outputs, consumed iff
+ *   *drew == 1 afterwards: the box is non-degenerate) or injected U (s x m).
+ *   Sums follow the OpenBLAS dgemv_t order of SURVEY App. A7.
+ * temo_hype_select: hype.py:153-163 on ranks from temo_rank (SELECT mode);
+ *   v_ref NULL = auto reference (hype.py:129-132); keep (n int32, lexsort
+ *   order); v_hv (N); info (4 int32) = {count(r<=l), k, estimated, drew}. */
+int temo_hype_alpha(int64_t n1, int64_t k, double *alpha, temo_stream_t stream);
+/* hype.auto_reference (hype.py:129-132); scratch: 32 doubles of device memory */
+int temo_auto_reference(const double *F, int64_t n, int m, double *out, double *scratch,
+                        temo_stream_t stream);
+size_t temo_hv_estimate_ws_bytes(int64_t n1, int m, int64_t s);
+int temo_hv_estimate(const double *F, int64_t n1, int m, const double *v_ref, int64_t k, int64_t s,
+                     const temo_philox_state *st, uint64_t off, const double *U, double *v_hv,
+                     int32_t *drew, void *ws, size_t ws_bytes, temo_stream_t stream);
+size_t temo_hype_select_ws_bytes(int64_t N, int m, int64_t s);
+int temo_hype_select(const double *F, int64_t N, int m, int64_t n, int64_t s, const double *v_ref,
+                     const int32_t *rank, const int32_t *l, const temo_philox_state *st,
+                     uint64_t off, const double *U, int32_t *keep, double *v_hv, int32_t *info,
+                     void *ws, size_t ws_bytes, temo_stream_t stream);
 
 /* --------------------------------------------------------------- directions
  * directions.neighbors (directions.py:104-114): out (r x T int32) holds the T

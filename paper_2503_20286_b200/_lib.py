@@ -53,6 +53,18 @@ SIGNATURES = {
     "temo_pm": (_I32, [_P, _P, _I64, _I64, _P, _U64, _P, _P, _P, _P]),
     "temo_offspring": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _U64, _P, _P, _P]),
     "temo_init_population": (_I32, [_P, _U64, _I64, _I64, _P, _P, _P, _P]),
+    "temo_moead_offspring": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _U64, _P, _P, _P]),
+    "temo_moead_compare": (_I32, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _D, _I32, _P, _P, _P, _P]),
+    "temo_moead_elite": (_I32, [_P, _P, _P, _P, _P, _I64, _I64, _I32, _I32, _P, _D, _I32, _P, _P, _P,
+                                _P, _P, _P, _P, _P]),
+    "temo_aggregate_rows": (_I32, [_P, _P, _P, _I64, _I32, _D, _I32, _I32, _P, _P]),
+    "temo_hype_alpha": (_I32, [_I64, _I64, _P, _P]),
+    "temo_auto_reference": (_I32, [_P, _I64, _I32, _P, _P, _P]),
+    "temo_hv_estimate_ws_bytes": (_SZ, [_I64, _I32, _I64]),
+    "temo_hv_estimate": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _P, _U64, _P, _P, _P, _P, _SZ, _P]),
+    "temo_hype_select_ws_bytes": (_SZ, [_I64, _I32, _I64]),
+    "temo_hype_select": (_I32, [_P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P,
+                                _SZ, _P]),
     "temo_probe_compare_rate": (_D, [_I32, _I32, _P]),
     "temo_timing_enable": (None, [_I32]),
     "temo_timing_name": (ctypes.c_char_p, [_I32]),

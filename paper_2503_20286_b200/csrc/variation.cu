@@ -178,7 +178,9 @@ __global__ void __launch_bounds__(VT) k_offspring(temo_problem P, VarArgs V, con
                                                   const int64_t *__restrict__ i1,
                                                   const int64_t *__restrict__ i2, int64_t h,
                                                   Philox ph, uint64_t off, double *__restrict__ O,
-                                                  double *__restrict__ FO, int smem_rows) {
+                                                  double *__restrict__ FO, int smem_rows, int single) {
+    // single != 0: MOEA/D mode (moead.py:136-144) -- keep child c1 only and mutate
+    // h rows, so the PM draws are (h, d) blocks instead of (2h, d)
     extern __shared__ double srow[];  // 2 x d children when smem_rows
     __shared__ double red[VT / 32];
     __shared__ double f[16];
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(VT) k_offspring(temo_problem P, VarArgs V, con
     const uint64_t hd = (uint64_t)h * d;
     const uint64_t o_mu = off, o_swap = off + hd, o_cross = off + (V.gene_swap ? 2 * hd : 0);
     const uint64_t o_pmu = off + (V.gene_swap ? 3 * hd : hd);
-    const uint64_t o_hit = o_pmu + 2 * hd;
+    const uint64_t o_hit = o_pmu + (single ? hd : 2 * hd);
     const double e = 1.0 / (V.eta_c + 1.0);
     const double eta = V.eta_m + 1.0;
     PhiloxCursor c_mu, c_sw, c_cr, c_pm1, c_pm2, c_h1, c_h2;
@@ -215,15 +217,15 @@ __global__ void __launch_bounds__(VT) k_offspring(temo_problem P, VarArgs V, con
             const uint64_t e1 = es, e2 = (uint64_t)(h + q) * d + g;
             if (V.p_m - c_h1.uniform(ph, o_hit + e1) >= 0.0)
                 c1 = pm_step(c1, lo, hi, c_pm1.uniform(ph, o_pmu + e1), eta);
-            if (V.p_m - c_h2.uniform(ph, o_hit + e2) >= 0.0)
-                c2 = pm_step(c2, lo, hi, c_pm2.uniform(ph, o_pmu + e2), eta);
             c1 = clipv(c1, lo, hi);
-            c2 = clipv(c2, lo, hi);
             o1[g] = c1;
-            o2[g] = c2;
-            if (smem_rows) {
-                srow[g] = c1;
-                srow[d + g] = c2;
+            if (smem_rows) srow[g] = c1;
+            if (!single) {
+                if (V.p_m - c_h2.uniform(ph, o_hit + e2) >= 0.0)
+                    c2 = pm_step(c2, lo, hi, c_pm2.uniform(ph, o_pmu + e2), eta);
+                c2 = clipv(c2, lo, hi);
+                o2[g] = c2;
+                if (smem_rows) srow[d + g] = c2;
             }
         }
     }
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(VT) k_offspring(temo_problem P, VarArgs V, con
     eval_row(P, r1, f, red);
     __syncthreads();
     if (threadIdx.x < P.m) FO[q * P.m + threadIdx.x] = f[threadIdx.x];
+    if (single) return;
     __syncthreads();
     eval_row(P, r2, f, red);
     __syncthreads();
@@ -375,13 +378,12 @@ extern "C" int temo_pm(const temo_variation *var, const double *X, int64_t rows,
     return TEMO_OK;
 }
 
-extern "C" int temo_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
-                              const int64_t *i1, const int64_t *i2, int64_t h,
-                              const temo_philox_state *st, uint64_t off, double *O, double *FO,
-                              temo_stream_t stream) {
+static int launch_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
+                            const int64_t *i1, const int64_t *i2, int64_t h,
+                            const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                            int single, cudaStream_t s) {
     if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !st || !O) return TEMO_EINVAL;
     if (h == 0) return TEMO_OK;
-    cudaStream_t s = (cudaStream_t)stream;
     const int64_t d = prob->d;
     int smem_rows = 2 * d * (int64_t)sizeof(double) <= 96 * 1024;
     const size_t smem = smem_rows ? 2 * d * sizeof(double) : 0;
@@ -389,10 +391,24 @@ extern "C" int temo_offspring(const temo_problem *prob, const temo_variation *va
         TEMO_CUDA(cudaFuncSetAttribute(k_offspring, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     stage_begin(S_OFFSPRING, s);
     k_offspring<<<(unsigned)h, VT, smem, s>>>(*prob, var_args(var), X, i1, i2, h, philox_from(*st),
-                                              off, O, FO, smem_rows);
+                                              off, O, FO, smem_rows, single);
     TEMO_LAUNCH_CHECK();
     stage_end(S_OFFSPRING, s);
     return TEMO_OK;
+}
+
+extern "C" int temo_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
+                              const int64_t *i1, const int64_t *i2, int64_t h,
+                              const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                              temo_stream_t stream) {
+    return launch_offspring(prob, var, X, i1, i2, h, st, off, O, FO, 0, (cudaStream_t)stream);
+}
+
+extern "C" int temo_moead_offspring(const temo_problem *prob, const temo_variation *var,
+                                    const double *X, const int64_t *p1, const int64_t *p2, int64_t n,
+                                    const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                                    temo_stream_t stream) {
+    return launch_offspring(prob, var, X, p1, p2, n, st, off, O, FO, 1, (cudaStream_t)stream);
 }
 
 extern "C" int temo_init_population(const temo_philox_state *st, uint64_t off, int64_t rows,

@@ -1,0 +1,106 @@
+"""CPU tests of the host-side logic (no GPU): RNG bridge, direction sets, problem descriptors."""
+
+import numpy as np
+import pytest
+
+from oracle import directions as odir
+from oracle import philox as ophilox
+from oracle import problems as oprob
+
+
+@pytest.mark.parametrize("pre", range(9))
+@pytest.mark.parametrize("count", [1, 2, 3, 4, 5, 7, 8, 9, 100, 1001])
+def test_rng_advance_equals_draws(pre, count):
+    from paper_2503_20286_b200.rng import advance
+
+    a = np.random.Generator(np.random.Philox(np.random.SeedSequence(3)))
+    b = np.random.Generator(np.random.Philox(np.random.SeedSequence(3)))
+    a.random(pre)
+    b.random(pre)
+    a.random(count)
+    advance(b, count)
+    assert np.array_equal(a.random(13), b.random(13))
+    assert np.array_equal(a.permutation(50), b.permutation(50))
+
+
+def test_device_draw_offsets_match_stream():
+    """DeviceDraws offsets index the same raw outputs the oracle's Philox restatement produces."""
+    from paper_2503_20286_b200.rng import DeviceDraws
+
+    g = np.random.Generator(np.random.Philox(np.random.SeedSequence(8)))
+    g.random(3)
+    st = g.bit_generator.state
+    dd = DeviceDraws(g)
+    o1 = dd.take(10)
+    o2 = dd.take(7)
+    assert (o1, o2) == (0, 10)
+    want = ophilox.doubles(st, 17)
+    dd.commit()
+    ref = np.random.Generator(np.random.Philox(np.random.SeedSequence(8)))
+    ref.random(3)
+    assert np.array_equal(ref.random(17), want)
+    assert np.array_equal(g.random(5), ref.random(5))
+
+
+@pytest.mark.parametrize("m,H", [(2, 40), (3, 12), (3, 630), (4, 7), (5, 6), (8, 3), (10, 3)])
+def test_simplex_lattice_and_lattice_H(m, H):
+    from paper_2503_20286_b200.directions import das_dennis, largest_h_for, simplex_lattice
+
+    W = simplex_lattice(m, H)
+    assert np.array_equal(W, odir.simplex_lattice(m, H))
+    assert das_dennis(m, H).lattice_H == H
+    assert largest_h_for(W.shape[0], m) == H
+
+
+def test_lattice_H_rejects_other_sets():
+    from paper_2503_20286_b200.directions import DirectionSet, das_dennis
+
+    W = das_dennis(3, 5).W.copy()
+    assert DirectionSet(W[::-1].copy(), "simplex").lattice_H == 0  # different row order
+    assert DirectionSet(W[:-1], "simplex").lattice_H == 0
+    assert DirectionSet(np.random.default_rng(0).random((10, 3)) + 0.1, "simplex").lattice_H == 0
+
+
+def test_lsmop_descriptor_matches_self_oracle():
+    from paper_2503_20286_b200.problems import lsmop_groups, make_problem
+
+    for m, d in ((3, 1000), (2, 300), (5, 700)):
+        a = lsmop_groups(m, d)
+        b = oprob.lsmop_groups(m, d)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        spec = make_problem("lsmop1", m=m, d=d)
+        lo, hi = oprob.lsmop_bounds(m, d)
+        assert np.array_equal(spec.lower, lo) and np.array_equal(spec.upper, hi)
+        s = spec.struct()
+        assert s.id == 101 and s.nk == 5 and s.sublen[0] == a[0][0]
+
+
+def test_run_config_validation():
+    from paper_2503_20286_b200.harness import ConfigError, RunConfig, _resolve
+
+    with pytest.raises(ConfigError):
+        RunConfig(algorithm="nope").validate()
+    with pytest.raises(ConfigError):
+        RunConfig(aggregation="x").validate()
+    spec, R, n = _resolve(RunConfig(algorithm="moead", problem="dtlz2", pop_size=100))
+    assert n == R.count == 91
+    spec, R, n = _resolve(RunConfig(algorithm="nsga3", problem="lsmop1", dim=1000, pop_size=200_000))
+    assert R.count == 199_396 and n == 200_000 and spec.d == 1000
+
+
+def test_moead_default_neighborhood():
+    from paper_2503_20286_b200.moead import default_neighborhood
+
+    assert default_neighborhood(10) == 2 and default_neighborhood(91) == 10 and default_neighborhood(1000) == 20
+
+
+def test_variation_params_validation():
+    from paper_2503_20286_b200.variation import VariationParams
+
+    with pytest.raises(ValueError):
+        VariationParams(eta_c=0.0, lower=np.zeros(2), upper=np.ones(2))
+    with pytest.raises(ValueError):
+        VariationParams(p_m=1.5, lower=np.zeros(2), upper=np.ones(2))
+    with pytest.raises(ValueError):
+        VariationParams(lower=np.ones(3), upper=np.zeros(3))
+    assert VariationParams(lower=np.zeros(4), upper=np.ones(4)).mutation_prob(4) == 0.25
