@@ -75,6 +75,31 @@ size_t temo_dominance_ws_bytes(int64_t N, int m);
 int temo_dominance(const double *F, int64_t N, int m, uint32_t *D_out, int32_t *status,
                    void *ws, size_t ws_bytes, temo_stream_t stream);
 
+/* --------------------------------------------------- column-sharded ND sort
+ * Multi-GPU form of temo_rank.  Every rank passes the same F;
+ * rank g owns sorted column tiles [jt_lo, jt_hi) from temo_rank_shard_bounds
+ * (multiples of 4 tiles of 256 columns; lo_hi receives 2G values, empty shards
+ * possible for tiny N).  Front step k, driven by the host:
+ *   temo_rank_shard_detect -> seg (8 (jt_hi - jt_lo) words: own front bits,
+ *                             sorted index space), count (device int32)
+ *   all-gather of the segments into the full mask (ceil(N/1024)*32 words)
+ *   temo_rank_shard_apply  -> ranks the whole front, subtracts its rows from
+ *                             the own columns' counts; front_total (device)
+ * and temo_rank_shard_finish writes ranks in the original row order (`fill`,
+ * a device int32, for rows never ranked in SELECT mode).  All calls of one
+ * shard share the workspace and (N, m, jt_lo, jt_hi). */
+void temo_rank_shard_bounds(int64_t N, int G, int64_t *lo_hi);
+size_t temo_rank_shard_ws_bytes(int64_t N, int m, int64_t jt_lo, int64_t jt_hi);
+int temo_rank_shard_build(const double *F, int64_t N, int m, int64_t jt_lo, int64_t jt_hi,
+                          int32_t *status, void *ws, size_t ws_bytes, temo_stream_t stream);
+int temo_rank_shard_detect(int64_t N, int m, int64_t jt_lo, int64_t jt_hi, uint32_t *seg,
+                           int32_t *count, void *ws, size_t ws_bytes, temo_stream_t stream);
+int temo_rank_shard_apply(int64_t N, int m, int64_t jt_lo, int64_t jt_hi, const uint32_t *full,
+                          int32_t k, int32_t *front_total, void *ws, size_t ws_bytes,
+                          temo_stream_t stream);
+int temo_rank_shard_finish(int64_t N, int m, int64_t jt_lo, int64_t jt_hi, const int32_t *fill,
+                           int32_t *rank, void *ws, size_t ws_bytes, temo_stream_t stream);
+
 /* ---------------------------------------------------------- NSGA-III select
  * Replaces nsga3.py:207-218 (normalize, associate, niche_counts, niche_select,
  * update_rank, keep) on already-shuffled objectives Fs (N x m) whose ranks

@@ -36,6 +36,12 @@ SIGNATURES = {
     "temo_rank": (_I32, [_P, _I64, _I32, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "temo_dominance_ws_bytes": (_SZ, [_I64, _I32]),
     "temo_dominance": (_I32, [_P, _I64, _I32, _P, _P, _P, _SZ, _P]),
+    "temo_rank_shard_bounds": (None, [_I64, _I32, _P]),
+    "temo_rank_shard_ws_bytes": (_SZ, [_I64, _I32, _I64, _I64]),
+    "temo_rank_shard_build": (_I32, [_P, _I64, _I32, _I64, _I64, _P, _P, _SZ, _P]),
+    "temo_rank_shard_detect": (_I32, [_I64, _I32, _I64, _I64, _P, _P, _P, _SZ, _P]),
+    "temo_rank_shard_apply": (_I32, [_I64, _I32, _I64, _I64, _P, _I32, _P, _P, _SZ, _P]),
+    "temo_rank_shard_finish": (_I32, [_I64, _I32, _I64, _I64, _P, _P, _P, _SZ, _P]),
     "temo_nsga3_select_ws_bytes": (_SZ, [_I64, _I32, _I64]),
     "temo_nsga3_select": (_I32, [_P, _I64, _I32, _P, _I64, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P,
                                  _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),

@@ -54,6 +54,8 @@ struct RankPlan {
     uint32_t *R;       // N x MP column ranks
     uint4 *rec;        // Np x NV records in lex order
     int64_t *rt_off;   // nT row-tile offsets into bits
+    int64_t *rt_lo;    // nT first stored word of each row tile
+    int64_t *rt_stride;  // nT words per row of each row tile
     uint32_t *bits;    // packed triangular bitmap
     int32_t *cnt, *rank_s, *list, *blkcnt;
     void *cub_tmp;
@@ -97,6 +99,8 @@ static void plan_rank(RankPlan &p, void *base, int64_t N, int m) {
     p.R = c.take<uint32_t>((size_t)N * 4 * p.NV);
     p.rec = c.take<uint4>((size_t)p.Np * p.NV);
     p.rt_off = c.take<int64_t>(p.nT);
+    p.rt_lo = c.take<int64_t>(p.nT);
+    p.rt_stride = c.take<int64_t>(p.nT);
     p.bits = c.take<uint32_t>((size_t)bitmap_words(p.nT, p.W));
     p.cnt = c.take<int32_t>(p.Np);
     p.rank_s = c.take<int32_t>(p.Np);
@@ -180,10 +184,12 @@ __global__ void k_records(const uint32_t *__restrict__ R, const int32_t *__restr
         rec[p * NV + v] = make_uint4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]);
 }
 
-__global__ void k_rowtile_offsets(int64_t nT, int64_t W, int64_t *off) {
+__global__ void k_rowtile_offsets(int64_t nT, int64_t W, int64_t *off, int64_t *lo, int64_t *stride) {
     int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (I >= nT) return;
     off[I] = (int64_t)TILE * (I * W - 8 * I * (I - 1) / 2);
+    lo[I] = 8 * I;
+    stride[I] = W - 8 * I;
 }
 
 // ------------------------------------------------------------------ K1
@@ -245,10 +251,21 @@ struct Transpose32 {
 // transposed across the warp and popcounted, which yields the dominated-by
 // counts of the 32 columns among the warp's 32 rows (the peel's initial
 // counts; no full-triangle counting pass).
+// Bitmap layout: columns tiles [jt_lo, jt_hi) are stored; row tile I keeps
+// words [lo_w[I], lo_w[I] + stride[I]) at bits + off[I] + r * stride[I].
+// The single-GPU triangle is jt_lo = 0, jt_hi = nT, lo_w = 8 I, stride = W - 8 I;
+// a column shard (multi-GPU) owns a contiguous [jt_lo, jt_hi).
+struct BitLayout {
+    int64_t jt_lo, jt_hi;
+    const int64_t *off;
+    const int64_t *lo_w;
+    const int64_t *stride;
+    int grid2d;  // 0: closed-form triangle items; 1: (chunk, strip) grid with early exit
+};
+
 template <int M>
 __global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec, int64_t N,
-                                                   int64_t nT, int64_t W,
-                                                   const int64_t *__restrict__ rt_off,
+                                                   int64_t nT, BitLayout L,
                                                    uint32_t *__restrict__ bits,
                                                    int32_t *__restrict__ cnt) {
     constexpr int NV = (M + 3) / 4;
@@ -260,18 +277,23 @@ __global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec
     __shared__ int32_t sCnt[TILE];
     __shared__ int64_t s_it, s_chunk;
     const int tid = threadIdx.x, lane = tid & 31;
-    if (tid == 0) {
-        // strip t = nT-1-I owns t+1 column tiles -> floor(t/CHUNK)+1 items
-        int64_t item = blockIdx.x, lo = 0, hi = nT - 1;
-        while (lo < hi) {
-            int64_t mid = (lo + hi + 1) >> 1;
-            if (items_before(mid) <= item) lo = mid; else hi = mid - 1;
+    if (!L.grid2d) {
+        if (tid == 0) {
+            // strip t = nT-1-I owns t+1 column tiles -> floor(t/CHUNK)+1 items
+            int64_t item = blockIdx.x, lo = 0, hi = nT - 1;
+            while (lo < hi) {
+                int64_t mid = (lo + hi + 1) >> 1;
+                if (items_before(mid) <= item) lo = mid; else hi = mid - 1;
+            }
+            s_it = nT - 1 - lo;
+            s_chunk = item - items_before(lo);
         }
-        s_it = nT - 1 - lo;
-        s_chunk = item - items_before(lo);
+        __syncthreads();
     }
-    __syncthreads();
-    const int64_t it = s_it, chunk = s_chunk;
+    const int64_t it = L.grid2d ? (int64_t)blockIdx.y : s_it;
+    const int64_t chunk = L.grid2d ? (int64_t)blockIdx.x : s_chunk;
+    const int64_t jstart = it > L.jt_lo ? it : L.jt_lo;  // first column tile of this strip
+    if (jstart + chunk * CHUNK >= L.jt_hi) return;      // (grid2d) empty item
     const int64_t i = it * TILE + tid;
     // own row: negated fields so that v + n = r(j) - r(i); id field: id(j) - id(i) - 1
     uint32_t nf[4 * NV];
@@ -286,8 +308,9 @@ __global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec
     const bool row_ok = i < N;
     const uint32_t last_i_id = fld(&rec[(it * TILE + TILE - 1) * NV], M - 1);
     const Transpose32 transpose(lane);
-    const int64_t jt0 = it + chunk * CHUNK;
-    const int64_t jt1 = min(jt0 + CHUNK, nT);
+    const int64_t jt0 = jstart + chunk * CHUNK;
+    const int64_t jt1 = min(jt0 + CHUNK, L.jt_hi);
+    const int64_t row_off = L.off[it], row_lo = L.lo_w[it], row_stride = L.stride[it];
     for (int64_t jt = jt0; jt < jt1; ++jt) {
         __syncthreads();
         uint4 rv[NV];
@@ -354,13 +377,13 @@ __global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec
         }
         __syncthreads();
         if (row_ok) {
-            uint32_t *dst = bits + rt_off[it] + (int64_t)tid * (W - 8 * it) + 8 * (jt - it);
+            uint32_t *dst = bits + row_off + (int64_t)tid * row_stride + (8 * jt - row_lo);
             const uint32_t *s = sB + tid * 9;
             reinterpret_cast<uint4 *>(dst)[0] = make_uint4(s[0], s[1], s[2], s[3]);
             reinterpret_cast<uint4 *>(dst)[1] = make_uint4(s[4], s[5], s[6], s[7]);
         }
         const int c = sCnt[tid];
-        if (c) atomicAdd(cnt + jt * TILE + tid, c);
+        if (c) atomicAdd(cnt + (jt - L.jt_lo) * TILE + tid, c);
     }
 }
 
@@ -608,8 +631,8 @@ __global__ void k_inverse(const int32_t *__restrict__ order, int64_t N, int32_t 
 // ------------------------------------------------------------------ host
 static inline dim3 grid1(int64_t n, int t = 256) { return dim3((unsigned)((n + t - 1) / t)); }
 
-// K0 + records + K1.  Leaves order in p.vals_a, records in p.rec, bitmap in p.bits.
-static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStream_t st) {
+// K0: column ranks, lex order (p.vals_a), run ids and records (p.rec)
+static int build_records(RankPlan &p, const double *F, int32_t *status, cudaStream_t st) {
     const int64_t N = p.N;
     const int m = p.m, MP = 4 * p.NV;
     size_t tb = p.cub_bytes;
@@ -639,17 +662,24 @@ static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStrea
     k_tuple_start<<<grid1(N), 256, 0, st>>>(p.R, p.vals_a, N, m, MP, p.scan_a);
     TEMO_CUDA(cub::DeviceScan::InclusiveScan(p.cub_tmp, tb, p.scan_a, p.scan_b, cub::Max(), (int)N, st));
     k_records<<<grid1(p.Np), 256, 0, st>>>(p.R, p.vals_a, p.scan_b, N, p.Np, m, MP, p.NV, p.rec);
-    k_rowtile_offsets<<<grid1(p.nT), 256, 0, st>>>(p.nT, p.W, p.rt_off);
     TEMO_LAUNCH_CHECK();
     stage_end(S_RANK_PREP, st);
-    // K1
+    return TEMO_OK;
+}
+
+// K1 over the column tiles of `L`; cnt (zeroed here) is indexed from column tile L.jt_lo
+static int launch_dom(int m, const uint4 *rec, int64_t N, int64_t nT, const BitLayout &L,
+                      uint32_t *bits, int32_t *cnt, cudaStream_t st) {
     stage_begin(S_DOM_BITS, st);
-    const int64_t items = p.nT + CHUNK * ((p.nT / CHUNK) * ((p.nT / CHUNK) - 1) / 2) +
-                          (p.nT % CHUNK) * (p.nT / CHUNK);
-    const dim3 g((unsigned)items);
-    TEMO_CUDA(cudaMemsetAsync(p.cnt, 0, sizeof(int32_t) * p.Np, st));
+    dim3 g;
+    if (L.grid2d) {
+        g = dim3((unsigned)((L.jt_hi - L.jt_lo + CHUNK - 1) / CHUNK), (unsigned)L.jt_hi);
+    } else {
+        g = dim3((unsigned)(nT + CHUNK * ((nT / CHUNK) * ((nT / CHUNK) - 1) / 2) + (nT % CHUNK) * (nT / CHUNK)));
+    }
+    TEMO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * TILE * (L.jt_hi - L.jt_lo), st));
 #define DOM_CASE(MM) \
-    case MM: k_dom_rows<MM><<<g, TILE, 0, st>>>(p.rec, N, p.nT, p.W, p.rt_off, p.bits, p.cnt); break;
+    case MM: k_dom_rows<MM><<<g, TILE, 0, st>>>(rec, N, nT, L, bits, cnt); break;
     switch (m) {
         DOM_CASE(1) DOM_CASE(2) DOM_CASE(3) DOM_CASE(4) DOM_CASE(5) DOM_CASE(6) DOM_CASE(7)
         DOM_CASE(8) DOM_CASE(9) DOM_CASE(10) DOM_CASE(11) DOM_CASE(12) DOM_CASE(13) DOM_CASE(14)
@@ -660,6 +690,15 @@ static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStrea
     TEMO_LAUNCH_CHECK();
     stage_end(S_DOM_BITS, st);
     return TEMO_OK;
+}
+
+// K0 + K1 on the full triangle.  Leaves order in p.vals_a, records in p.rec, bitmap in p.bits.
+static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStream_t st) {
+    int rc = build_records(p, F, status, st);
+    if (rc) return rc;
+    k_rowtile_offsets<<<grid1(p.nT), 256, 0, st>>>(p.nT, p.W, p.rt_off, p.rt_lo, p.rt_stride);
+    BitLayout L{0, p.nT, p.rt_off, p.rt_lo, p.rt_stride, 0};
+    return launch_dom(p.m, p.rec, p.N, p.nT, L, p.bits, p.cnt, st);
 }
 
 static int peel_grid(int NB, size_t smem) {
@@ -747,3 +786,5 @@ extern "C" int temo_dominance(const double *F, int64_t N, int m, uint32_t *D_out
     TEMO_LAUNCH_CHECK();
     return TEMO_OK;
 }
+
+#include "ndsort_shard.cuh"

@@ -134,7 +134,14 @@ class _Stepper:
         self.perm = t.empty(self.N, dtype=t.int64, device=self.dev)
         alg = config.algorithm
         if alg == "nsga3":
-            self.selector = Nsga3Selector(self.N, m, R, n, self.dev)
+            dist_rank = None
+            import torch.distributed as dist
+
+            if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+                from .parallel import DistRank
+
+                dist_rank = DistRank(self.N, m, dist.get_rank(), dist.get_world_size(), self.dev)
+            self.selector = Nsga3Selector(self.N, m, R, n, self.dev, dist_rank=dist_rank)
         elif alg == "hype":
             from .hype import HypeSelector
 

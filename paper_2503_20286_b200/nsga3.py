@@ -164,9 +164,11 @@ class Nsga3Selector:
     indices into the shuffled order (ascending), like ``flatnonzero(rank < l)``.
     """
 
-    def __init__(self, N: int, m: int, R: DirectionSet, n: int, dev=None, record=False, lattice=True):
+    def __init__(self, N: int, m: int, R: DirectionSet, n: int, dev=None, record=False, lattice=True,
+                 dist_rank=None):
         t = _t()
         self.lattice_H = R.lattice_H if lattice else 0
+        self.dist_rank = dist_rank  # parallel.DistRank: column-sharded ND sort across ranks
         self.dev = _lib.device(dev)
         self.N, self.m, self.n = N, m, n
         self.R = R
@@ -197,7 +199,13 @@ class Nsga3Selector:
         """Run on ``self.Fs`` (or copy ``Fs`` in first); returns the keep tensor."""
         if Fs is not None:
             self.Fs.copy_(Fs)
-        rank_device(self.Fs, self.n, SELECT, self.status, out=(self.rank, self.l, self.nfronts))
+        if self.dist_rank is not None:
+            r, l, nf = self.dist_rank(self.Fs, self.n, SELECT)
+            self.rank.copy_(r)
+            self.l.fill_(l)
+            self.nfronts.fill_(nf)
+        else:
+            rank_device(self.Fs, self.n, SELECT, self.status, out=(self.rank, self.l, self.nfronts))
         L = _lib.lib()
         ws = _lib.workspace.get(self.ws_sel, self.dev)
         p = _lib.ptr

@@ -1,0 +1,186 @@
+"""Multi-GPU ND sort: column-sharded dominance with a per-front mask all-gather.
+
+One process per GPU (``torch.distributed``, NCCL over NVLink).  Every rank
+holds the same objectives F, runs K0 identically and owns a contiguous range
+of sorted column tiles (``shard_bounds``: equal triangle area).  K1 builds only
+the rank's bitmap columns and their dominated-by counts -- no exchange.  Each
+front step exchanges one N-bit mask:
+
+    detect (own columns)  ->  all-gather of the mask segments  ->  apply (rank the
+    front everywhere, subtract its rows from the own columns' counts)
+
+``run_sharded`` is written against two small interfaces -- a backend
+(``CudaShardBackend`` here; a NumPy backend in tests) and an exchange
+(``TorchDistExchange`` for NCCL/gloo, ``LockstepExchange`` to run G shards in one
+process) -- so the orchestration is tested on CPU with gloo and the kernels on
+one GPU with simulated shards.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+SORT, SELECT = 0, 1
+
+
+def shard_bounds(N: int, G: int):
+    """[(jt_lo, jt_hi)] column-tile ranges (256 sorted columns per tile) for G shards."""
+    out = np.zeros(2 * G, dtype=np.int64)
+    _lib.lib().temo_rank_shard_bounds(N, G, _lib._P(out.ctypes.data))
+    return [(int(out[2 * g]), int(out[2 * g + 1])) for g in range(G)]
+
+
+def mask_words(N: int) -> int:
+    """Words of the full front mask (sorted index space, padded to 1024 rows)."""
+    return ((N + 1023) // 1024) * 32
+
+
+class CudaShardBackend:
+    """One rank's shard of the sorted columns on its GPU (C ABI temo_rank_shard_*)."""
+
+    def __init__(self, N: int, m: int, lo: int, hi: int, dev=None):
+        t = _lib.torch()
+        self.N, self.m, self.lo, self.hi = N, m, lo, hi
+        self.dev = _lib.device(dev)
+        self.empty = hi <= lo
+        self.seg = t.zeros(max(8 * (hi - lo), 1), dtype=t.int32, device=self.dev)
+        self.count = t.zeros(1, dtype=t.int32, device=self.dev)
+        self.total = t.zeros(1, dtype=t.int32, device=self.dev)
+        self.fill = t.zeros(1, dtype=t.int32, device=self.dev)
+        self.rank = t.empty(N, dtype=t.int32, device=self.dev)
+        self.status = t.zeros(1, dtype=t.int32, device=self.dev)
+        L = _lib.lib()
+        # empty shards still need K0 + rank bookkeeping: give them a one-block dummy range
+        self.plo, self.phi = (lo, hi) if not self.empty else (0, 4)
+        self.ws = t.empty(L.temo_rank_shard_ws_bytes(N, m, self.plo, self.phi), dtype=t.uint8,
+                          device=self.dev)
+        self._empty_seg = t.zeros(1, dtype=t.int32, device=self.dev)
+
+    def _a(self):
+        return (self.N, self.m, self.plo, self.phi)
+
+    def build(self, Fd):
+        L = _lib.lib()
+        rc = L.temo_rank_shard_build(_lib.ptr(Fd), self.N, self.m, self.plo, self.phi, _lib.ptr(self.status),
+                                     _lib.ptr(self.ws), self.ws.numel(), _lib.stream_handle(self.dev))
+        _lib.check(rc, "rank_shard_build")
+
+    def detect(self, k: int):
+        if self.empty:
+            return self.seg[:0], self.count
+        rc = _lib.lib().temo_rank_shard_detect(*self._a(), _lib.ptr(self.seg), _lib.ptr(self.count),
+                                               _lib.ptr(self.ws), self.ws.numel(),
+                                               _lib.stream_handle(self.dev))
+        _lib.check(rc, "rank_shard_detect")
+        return self.seg, self.count
+
+    def apply(self, full, k: int):
+        rc = _lib.lib().temo_rank_shard_apply(*self._a(), _lib.ptr(full), int(k), _lib.ptr(self.total),
+                                              _lib.ptr(self.ws), self.ws.numel(),
+                                              _lib.stream_handle(self.dev))
+        _lib.check(rc, "rank_shard_apply")
+        return self.total
+
+    def finish(self, fill: int):
+        self.fill.fill_(int(fill))
+        rc = _lib.lib().temo_rank_shard_finish(*self._a(), _lib.ptr(self.fill), _lib.ptr(self.rank),
+                                               _lib.ptr(self.ws), self.ws.numel(),
+                                               _lib.stream_handle(self.dev))
+        _lib.check(rc, "rank_shard_finish")
+        return self.rank
+
+
+class TorchDistExchange:
+    """All-gather of per-rank mask segments through torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, bounds, W: int, device, group=None):
+        t = _lib.torch()
+        self.bounds = bounds
+        self.W = W
+        self.S = max(max(8 * (hi - lo) for lo, hi in bounds), 1)
+        self.group = group
+        self.send = t.zeros(self.S, dtype=t.int32, device=device)
+        self.recv = t.zeros(len(bounds) * self.S, dtype=t.int32, device=device)
+        self.full = t.zeros(W, dtype=t.int32, device=device)
+
+    def __call__(self, seg):
+        import torch.distributed as dist
+
+        self.send.zero_()
+        self.send[: seg.numel()].copy_(seg)
+        dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        for g, (lo, hi) in enumerate(self.bounds):
+            n = 8 * (hi - lo)
+            if n:
+                self.full[8 * lo: 8 * hi].copy_(self.recv[g * self.S: g * self.S + n])
+        return self.full
+
+
+def assemble(bounds, segs, W, like):
+    """Full mask from per-shard segments (used by the lockstep exchange and tests)."""
+    full = like.new_zeros(W)
+    for (lo, hi), seg in zip(bounds, segs):
+        if hi > lo:
+            full[8 * lo: 8 * hi] = seg[: 8 * (hi - lo)]
+    return full
+
+
+def run_sharded(backend, exchange, N: int, n: int, mode: int = SORT):
+    """Front loop of one rank; returns (rank in original order, l, number of fronts)."""
+    k, ranked, l = 0, 0, -1
+    while True:
+        seg, _ = backend.detect(k)
+        full = exchange(seg)
+        total = int(backend.apply(full, k).item())
+        if total == 0:
+            if ranked < N:
+                raise RuntimeError("front peeling failed to terminate")
+            break
+        ranked += total
+        if l < 0 and ranked >= n:
+            l = k
+        k += 1
+        if (mode == SELECT and ranked >= n) or ranked >= N:
+            break
+    return backend.finish(l + 1), l, k
+
+
+def run_lockstep(backends, bounds, N: int, n: int, mode: int = SORT):
+    """G shards in one process, advanced together (single-GPU test of the shard kernels)."""
+    k, ranked, l = 0, 0, -1
+    W = mask_words(N)
+    while True:
+        segs = [b.detect(k)[0] for b in backends]
+        full = assemble(bounds, segs, W, segs[0] if segs[0].numel() else backends[0].seg)
+        totals = [int(b.apply(full, k).item()) for b in backends]
+        assert len(set(totals)) == 1
+        total = totals[0]
+        if total == 0:
+            if ranked < N:
+                raise RuntimeError("front peeling failed to terminate")
+            break
+        ranked += total
+        if l < 0 and ranked >= n:
+            l = k
+        k += 1
+        if (mode == SELECT and ranked >= n) or ranked >= N:
+            break
+    return [b.finish(l + 1) for b in backends], l, k
+
+
+class DistRank:
+    """Sharded replacement of ``rank_device`` for one rank of a process group."""
+
+    def __init__(self, N: int, m: int, rank: int, world: int, dev=None, group=None):
+        self.N, self.m = N, m
+        self.bounds = shard_bounds(N, world)
+        lo, hi = self.bounds[rank]
+        self.backend = CudaShardBackend(N, m, lo, hi, dev)
+        self.exchange = TorchDistExchange(self.bounds, mask_words(N), self.backend.dev, group)
+
+    def __call__(self, Fd, n: int, mode: int = SELECT):
+        self.backend.build(Fd)
+        rank, l, nf = run_sharded(self.backend, self.exchange, self.N, n, mode)
+        return rank, l, nf
