@@ -648,6 +648,7 @@ static int build_records(RankPlan &p, const double *F, int32_t *status, cudaStre
     }
     // lexicographic order of rank tuples: LSD passes, several columns per u64 key
     k_iota<<<grid1(N), 256, 0, st>>>(p.vals_a, N);
+    int32_t *const va0 = p.vals_a, *const vb0 = p.vals_b;
     const int per = 64 / p.bitsN;
     for (int hi = m; hi > 0;) {
         const int g = hi < per ? hi : per;
@@ -657,6 +658,11 @@ static int build_records(RankPlan &p, const double *F, int32_t *status, cudaStre
                                                   p.vals_b, (int)N, 0, g * p.bitsN, st));
         std::swap(p.vals_a, p.vals_b);
         hi = c0;
+    }
+    if (p.vals_a != va0) {  // keep the order in the plan's canonical buffer (re-planned calls read it)
+        TEMO_CUDA(cudaMemcpyAsync(va0, p.vals_a, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st));
+        p.vals_a = va0;
+        p.vals_b = vb0;
     }
     // run ids of equal tuples
     k_tuple_start<<<grid1(N), 256, 0, st>>>(p.R, p.vals_a, N, m, MP, p.scan_a);
