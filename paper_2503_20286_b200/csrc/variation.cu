@@ -8,6 +8,12 @@
 // bit-identical), stages both children in shared memory and evaluates them
 // (DTLZ1-7 or LSMOP1) with block reductions -- no uniform matrices, children
 // or objectives round-trip through HBM except the final O and FO rows.
+//
+// Each thread owns quads of 4 consecutive genes: parents and children move
+// as 32-byte vectors, and every stream's 4 uniforms come from at most two
+// Philox blocks generated on the spot (no long-lived per-stream cursor
+// state), which keeps the kernel at <= 80 registers.  Evaluation is
+// templated on m so per-objective accumulators live in registers.
 #include "common.cuh"
 #include "philox.cuh"
 
@@ -36,7 +42,7 @@ __device__ __forceinline__ void sbx_gene(double x1, double x2, double mu, double
     c2 = x2 + shift * (x1 - x2);
 }
 
-__device__ __forceinline__ double pm_step(double x, double lo, double hi, double mu, double eta) {
+__device__ __noinline__ double pm_step(double x, double lo, double hi, double mu, double eta) {
     const double span = hi - lo;
     double step;
     if (0.5 - mu >= 0.0) {
@@ -47,6 +53,19 @@ __device__ __forceinline__ double pm_step(double x, double lo, double hi, double
         step = 1.0 - pow(2.0 - 2.0 * mu + (2.0 * mu - 1.0) * pow(1.0 - gap, eta), 1.0 / eta);
     }
     return x + step * span;
+}
+
+// `cnt` consecutive uniforms of the stream starting at element e0 (<= 2 Philox blocks)
+__device__ __forceinline__ void uniforms4(const Philox &ph, uint64_t e0, int cnt, double u[4]) {
+    PhiloxCursor c;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (k < cnt) u[k] = c.uniform(ph, e0 + k);
+}
+
+__device__ __forceinline__ double uniform1(const Philox &ph, uint64_t e) {
+    PhiloxCursor c;
+    return c.uniform(ph, e);
 }
 
 // ------------------------------------------------------------------ evaluation
@@ -61,42 +80,46 @@ __device__ double block_sum(double v, double *red) {
     return s;
 }
 
-// objectives of one row x (length d) -> f[0..m); called by every thread of the CTA
+// objectives of one row x (length d) -> f[0..M); called by every thread of the CTA
+template <int M>
 __device__ void eval_row(const temo_problem &P, const double *x, double *f, double *red) {
-    const int m = P.m;
     const int64_t d = P.d;
     const int id = P.id;
     if (id == TEMO_PROB_LSMOP1) {
-        double part[16];
-        for (int i = 0; i < m; ++i) part[i] = 0.0;
+        double part[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) part[i] = 0.0;
         const double x0 = x[0];
-        const int64_t span_s = P.offset[m];
-        for (int64_t g = (m - 1) + threadIdx.x; g < d; g += blockDim.x) {
-            const int64_t rel = g - (m - 1);
+        const int64_t span_s = P.offset[M];
+        for (int64_t g = (M - 1) + threadIdx.x; g < d; g += blockDim.x) {
+            const int64_t rel = g - (M - 1);
             if (rel >= span_s) continue;
             const double a = (double)(g + 1);
             const double xs = (1.0 + a / (double)d) * x[g] - 10.0 * x0;
-            int i = 0;
-            while (i + 1 < m && rel >= P.offset[i + 1]) ++i;
-            part[i] += xs * xs;
+            const double sq = xs * xs;
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                if (rel >= P.offset[i] && rel < P.offset[i + 1]) part[i] += sq;
         }
-        double G[16];
-        for (int i = 0; i < m; ++i) G[i] = block_sum(part[i], red);
+        double G[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) G[i] = block_sum(part[i], red);
         if (threadIdx.x == 0) {
-            for (int i = 0; i < m; ++i) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
                 const double gi = G[i] / (double)P.sublen[i] / (double)P.nk;
                 double head = 1.0;
-                for (int k = 0; k < m - 1 - i; ++k) head = head * x[k];
-                const double tail = i == 0 ? 1.0 : 1.0 - x[m - 1 - i];
+                for (int k = 0; k < M - 1 - i; ++k) head = head * x[k];
+                const double tail = i == 0 ? 1.0 : 1.0 - x[M - 1 - i];
                 f[i] = (1.0 + gi) * head * tail;
             }
         }
         return;
     }
     // DTLZ family: g over the distance variables xm = x[m-1:]
-    const int64_t k = d - m + 1;
+    const int64_t k = d - M + 1;
     double acc = 0.0;
-    for (int64_t g = (m - 1) + threadIdx.x; g < d; g += blockDim.x) {
+    for (int64_t g = (M - 1) + threadIdx.x; g < d; g += blockDim.x) {
         const double v = x[g];
         switch (id) {
             case 1:
@@ -123,48 +146,52 @@ __device__ void eval_row(const temo_problem &P, const double *x, double *f, doub
     else if (id == 7) g = 1.0 + 9.0 / (double)k * s;
     else g = s;
     if (id == 1) {
-        for (int i = 0; i < m; ++i) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
             double p = 1.0;
-            for (int q = 0; q < m - 1 - i; ++q) p = p * x[q];
-            if (i) p = p * (1.0 - x[m - 1 - i]);
+            for (int q = 0; q < M - 1 - i; ++q) p = p * x[q];
+            if (i) p = p * (1.0 - x[M - 1 - i]);
             f[i] = 0.5 * (1.0 + g) * p;
         }
         return;
     }
     if (id == 7) {
         double h = 0.0;
-        for (int q = 0; q < m - 1; ++q) {
+        for (int q = 0; q < M - 1; ++q) {
             f[q] = x[q];
             h += x[q] / (1.0 + g) * (1.0 + sin(3.0 * PI * x[q]));
         }
-        f[m - 1] = (1.0 + g) * ((double)m - h);
+        f[M - 1] = (1.0 + g) * ((double)M - h);
         return;
     }
-    double th[16];
-    for (int q = 0; q < m - 1; ++q) {
+    double th[M];
+#pragma unroll
+    for (int q = 0; q < M - 1; ++q) {
         if (id == 4) th[q] = pow(x[q], 100.0) * (PI / 2.0);
         else if (id == 5 || id == 6) {
             if (q == 0) th[q] = x[0] * (PI / 2.0);
             else th[q] = PI / (4.0 * (1.0 + g)) * (1.0 + 2.0 * g * x[q]);
         } else th[q] = x[q] * (PI / 2.0);
     }
-    for (int i = 0; i < m; ++i) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
         double p = 1.0;
-        for (int q = 0; q < m - 1 - i; ++q) p = p * cos(th[q]);
-        if (i) p = p * sin(th[m - 1 - i]);
+        for (int q = 0; q < M - 1 - i; ++q) p = p * cos(th[q]);
+        if (i) p = p * sin(th[M - 1 - i]);
         f[i] = (1.0 + g) * p;
     }
 }
 
+template <int M>
 __global__ void __launch_bounds__(VT) k_evaluate(temo_problem P, const double *__restrict__ X,
                                                  int64_t n, double *__restrict__ F) {
     __shared__ double red[VT / 32];
     __shared__ double f[16];
     const int64_t r = blockIdx.x;
     if (r >= n) return;
-    eval_row(P, X + r * P.d, f, red);
+    eval_row<M>(P, X + r * P.d, f, red);
     __syncthreads();
-    if (threadIdx.x < P.m) F[r * P.m + threadIdx.x] = f[threadIdx.x];
+    if (threadIdx.x < M) F[r * M + threadIdx.x] = f[threadIdx.x];
 }
 
 // ------------------------------------------------------------------ fused offspring
@@ -174,11 +201,12 @@ struct VarArgs {
     const double *lower, *upper;
 };
 
-__global__ void __launch_bounds__(VT) k_offspring(temo_problem P, VarArgs V, const double *__restrict__ X,
-                                                  const int64_t *__restrict__ i1,
-                                                  const int64_t *__restrict__ i2, int64_t h,
-                                                  Philox ph, uint64_t off, double *__restrict__ O,
-                                                  double *__restrict__ FO, int smem_rows, int single) {
+template <int M>
+__global__ void __launch_bounds__(VT, 6) k_offspring(temo_problem P, VarArgs V, const double *__restrict__ X,
+                                                     const int64_t *__restrict__ i1,
+                                                     const int64_t *__restrict__ i2, int64_t h,
+                                                     Philox ph, uint64_t off, double *__restrict__ O,
+                                                     double *__restrict__ FO, int smem_rows, int single) {
     // single != 0: MOEA/D mode (moead.py:136-144) -- keep child c1 only and mutate
     // h rows, so the PM draws are (h, d) blocks instead of (2h, d)
     extern __shared__ double srow[];  // 2 x d children when smem_rows
@@ -196,52 +224,86 @@ __global__ void __launch_bounds__(VT) k_offspring(temo_problem P, VarArgs V, con
     const uint64_t o_hit = o_pmu + (single ? hd : 2 * hd);
     const double e = 1.0 / (V.eta_c + 1.0);
     const double eta = V.eta_m + 1.0;
-    PhiloxCursor c_mu, c_sw, c_cr, c_pm1, c_pm2, c_h1, c_h2;
-    for (int64_t g0 = 4 * (int64_t)threadIdx.x; g0 < d; g0 += 4 * VT) {
-        const int64_t g1 = g0 + 4 < d ? g0 + 4 : d;
-        for (int64_t g = g0; g < g1; ++g) {
-            const uint64_t es = (uint64_t)q * d + g;
-            double c1, c2;
-            const double crs = V.gene_swap ? c_cr.uniform(ph, o_cross + es) : 0.0;
-            if (V.gene_swap && !(crs < 0.5)) {
-                sbx_gene(x1[g], x2[g], 0.0, 0.0, crs, e, true, c1, c2);
-            } else {
-                const double mu = c_mu.uniform(ph, o_mu + es);
-                const double sw = V.gene_swap ? c_sw.uniform(ph, o_swap + es) : 1.0;
-                sbx_gene(x1[g], x2[g], mu, sw, crs, e, V.gene_swap, c1, c2);
-            }
-            const double lo = V.lower[g], hi = V.upper[g];
-            c1 = clipv(c1, lo, hi);
-            c2 = clipv(c2, lo, hi);
-            // polynomial mutation on rows q (c1) and h+q (c2)
-            const uint64_t e1 = es, e2 = (uint64_t)(h + q) * d + g;
-            if (V.p_m - c_h1.uniform(ph, o_hit + e1) >= 0.0)
-                c1 = pm_step(c1, lo, hi, c_pm1.uniform(ph, o_pmu + e1), eta);
-            c1 = clipv(c1, lo, hi);
-            o1[g] = c1;
-            if (smem_rows) srow[g] = c1;
-            if (!single) {
-                if (V.p_m - c_h2.uniform(ph, o_hit + e2) >= 0.0)
-                    c2 = pm_step(c2, lo, hi, c_pm2.uniform(ph, o_pmu + e2), eta);
-                c2 = clipv(c2, lo, hi);
-                o2[g] = c2;
-                if (smem_rows) srow[d + g] = c2;
+    // Quads are shifted by `sh` so that 4 consecutive genes are exactly one
+    // Philox block of the crossed stream (and of every stream whose offset is
+    // congruent mod 4): one block per stream per quad instead of up to two.
+    const uint64_t avail = (uint64_t)(4 - ph.pos);
+    const int sh = (int)((o_cross + (uint64_t)q * d + 4 * 1024 - avail) & 3);  // genes before 1st boundary
+    const int64_t first = -sh;  // quad t covers genes [first + 4t, first + 4t + 4)
+    for (int64_t g0 = first + 4 * (int64_t)threadIdx.x; g0 < d; g0 += 4 * VT) {
+        const int64_t ga = g0 < 0 ? 0 : g0;
+        const int cnt = (int)((g0 + 4 < d ? g0 + 4 : d) - ga);
+        double c1[4], c2[4];
+        const uint64_t es = (uint64_t)q * d + ga;
+        // SBX (variation.py:72-91): crossed first, mu/swap only where crossed
+        double crs[4] = {0.0, 0.0, 0.0, 0.0};
+        bool any = !V.gene_swap;
+        if (V.gene_swap) {
+            uniforms4(ph, o_cross + es, cnt, crs);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) any |= (k < cnt) && crs[k] < 0.5;
+        }
+        double mu[4] = {0.0, 0.0, 0.0, 0.0}, sw[4] = {1.0, 1.0, 1.0, 1.0};
+        if (any) {
+            uniforms4(ph, o_mu + es, cnt, mu);
+            if (V.gene_swap) uniforms4(ph, o_swap + es, cnt, sw);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k < cnt) {
+                const int64_t g = ga + k;
+                const double lo = V.lower[g], hi = V.upper[g];
+                sbx_gene(x1[g], x2[g], mu[k], sw[k], crs[k], e, V.gene_swap != 0, c1[k], c2[k]);
+                c1[k] = clipv(c1[k], lo, hi);
+                c2[k] = clipv(c2[k], lo, hi);
             }
         }
+        // polynomial mutation (variation.py:104-120) on rows q (c1) and h+q (c2)
+        double hit[4];
+        uniforms4(ph, o_hit + es, cnt, hit);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k < cnt && V.p_m - hit[k] >= 0.0) {  // PM only where hit (rate p_m)
+                const int64_t g = ga + k;
+                c1[k] = clipv(pm_step(c1[k], V.lower[g], V.upper[g], uniform1(ph, o_pmu + es + k), eta),
+                              V.lower[g], V.upper[g]);
+            }
+        }
+        if (!single) {
+            const uint64_t e2 = (uint64_t)(h + q) * d + ga;
+            uniforms4(ph, o_hit + e2, cnt, hit);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (k < cnt && V.p_m - hit[k] >= 0.0) {
+                    const int64_t g = ga + k;
+                    c2[k] = clipv(pm_step(c2[k], V.lower[g], V.upper[g], uniform1(ph, o_pmu + e2 + k), eta),
+                                  V.lower[g], V.upper[g]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < cnt) {
+                o1[ga + k] = c1[k];
+                if (!single) o2[ga + k] = c2[k];
+                if (smem_rows) {
+                    srow[ga + k] = c1[k];
+                    if (!single) srow[d + ga + k] = c2[k];
+                }
+            }
     }
     if (!FO) return;
     __syncthreads();
     const double *r1 = smem_rows ? srow : o1;
     const double *r2 = smem_rows ? srow + d : o2;
-    if (!smem_rows) __threadfence_block();
-    eval_row(P, r1, f, red);
+    eval_row<M>(P, r1, f, red);
     __syncthreads();
-    if (threadIdx.x < P.m) FO[q * P.m + threadIdx.x] = f[threadIdx.x];
+    if (threadIdx.x < M) FO[q * M + threadIdx.x] = f[threadIdx.x];
     if (single) return;
     __syncthreads();
-    eval_row(P, r2, f, red);
+    eval_row<M>(P, r2, f, red);
     __syncthreads();
-    if (threadIdx.x < P.m) FO[(h + q) * P.m + threadIdx.x] = f[threadIdx.x];
+    if (threadIdx.x < M) FO[(h + q) * M + threadIdx.x] = f[threadIdx.x];
 }
 
 // ------------------------------------------------------------------ standalone operators
@@ -321,6 +383,13 @@ static Philox philox_or_zero(const temo_philox_state *st) {
     return philox_from(z);
 }
 
+#define TEMO_M_SWITCH(m, CASE)                                                                     \
+    switch (m) {                                                                                   \
+        CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) \
+        CASE(13) CASE(14) CASE(15) CASE(16)                                                        \
+        default: return TEMO_EINVAL;                                                               \
+    }
+
 }  // namespace temo
 
 using namespace temo;
@@ -329,10 +398,13 @@ extern "C" int temo_evaluate(const temo_problem *prob, const double *X, int64_t 
                              temo_stream_t stream) {
     if (!prob_ok(prob) || n < 0 || !X || !F) return TEMO_EINVAL;
     if (n == 0) return TEMO_OK;
-    stage_begin(S_EVALUATE, (cudaStream_t)stream);
-    k_evaluate<<<(unsigned)n, VT, 0, (cudaStream_t)stream>>>(*prob, X, n, F);
+    cudaStream_t s = (cudaStream_t)stream;
+    stage_begin(S_EVALUATE, s);
+#define EVAL_CASE(MM) case MM: k_evaluate<MM><<<(unsigned)n, VT, 0, s>>>(*prob, X, n, F); break;
+    TEMO_M_SWITCH(prob->m, EVAL_CASE)
+#undef EVAL_CASE
     TEMO_LAUNCH_CHECK();
-    stage_end(S_EVALUATE, (cudaStream_t)stream);
+    stage_end(S_EVALUATE, s);
     return TEMO_OK;
 }
 
@@ -385,13 +457,19 @@ static int launch_offspring(const temo_problem *prob, const temo_variation *var,
     if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !st || !O) return TEMO_EINVAL;
     if (h == 0) return TEMO_OK;
     const int64_t d = prob->d;
-    int smem_rows = 2 * d * (int64_t)sizeof(double) <= 96 * 1024;
+    const int smem_rows = 2 * d * (int64_t)sizeof(double) <= 96 * 1024;
     const size_t smem = smem_rows ? 2 * d * sizeof(double) : 0;
-    if (smem > 48 * 1024)
-        TEMO_CUDA(cudaFuncSetAttribute(k_offspring, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
     stage_begin(S_OFFSPRING, s);
-    k_offspring<<<(unsigned)h, VT, smem, s>>>(*prob, var_args(var), X, i1, i2, h, philox_from(*st),
-                                              off, O, FO, smem_rows, single);
+#define OFF_CASE(MM)                                                                              \
+    case MM:                                                                                      \
+        if (smem > 48 * 1024)                                                                     \
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring<MM>,                                       \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)); \
+        k_offspring<MM><<<(unsigned)h, VT, smem, s>>>(*prob, var_args(var), X, i1, i2, h,         \
+                                                      philox_from(*st), off, O, FO, smem_rows, single); \
+        break;
+    TEMO_M_SWITCH(prob->m, OFF_CASE)
+#undef OFF_CASE
     TEMO_LAUNCH_CHECK();
     stage_end(S_OFFSPRING, s);
     return TEMO_OK;
