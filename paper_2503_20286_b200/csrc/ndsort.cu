@@ -53,6 +53,8 @@ struct RankPlan {
     int32_t *vals_a, *vals_b, *scan_a, *scan_b;
     uint32_t *R;       // N x MP column ranks
     uint4 *rec;        // Np x NV records in lex order
+    uint32_t *lsorted; // K1 packed: sorted local rank fields per column super-tile
+    uint32_t *qpk;     // K1 packed: column-pair local ranks, 16-bit halves
     int64_t *rt_off;   // nT row-tile offsets into bits
     int64_t *rt_lo;    // nT first stored word of each row tile
     int64_t *rt_stride;  // nT words per row of each row tile
@@ -77,6 +79,14 @@ static size_t cub_need(int64_t N) {
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 
+// K1 packed-path buffers (sizes in k_local_ranks / k_dom_packed)
+static void take_packed(RankPlan &p, Carve &c) {
+    const int64_t K = (p.nT + 7) / 8;  // 2048-column super-tiles
+    const int FD = p.m > 1 ? p.m - 1 : 1;
+    p.lsorted = c.take<uint32_t>((size_t)K * FD * 2048);
+    p.qpk = c.take<uint32_t>((size_t)p.nT * 128 * FD);
+}
+
 static void plan_rank(RankPlan &p, void *base, int64_t N, int m) {
     p.N = N;
     p.m = m;
@@ -98,6 +108,7 @@ static void plan_rank(RankPlan &p, void *base, int64_t N, int m) {
     p.scan_b = c.take<int32_t>(N);
     p.R = c.take<uint32_t>((size_t)N * 4 * p.NV);
     p.rec = c.take<uint4>((size_t)p.Np * p.NV);
+    take_packed(p, c);
     p.rt_off = c.take<int64_t>(p.nT);
     p.rt_lo = c.take<int64_t>(p.nT);
     p.rt_stride = c.take<int64_t>(p.nT);
@@ -387,6 +398,210 @@ __global__ void __launch_bounds__(TILE) k_dom_rows(const uint4 *__restrict__ rec
     }
 }
 
+// ---------------------------------------------------------- K1 (packed)
+// Two columns per integer subtraction.  Column super-tiles of SUPER = 2048
+// sorted columns (8 tiles) get LOCAL ranks per rank field k:
+//     q_k(j) = #{j' in super-tile : r_k(j') < r_k(j)}      (column side)
+//     p_k(i) = #{j' in super-tile : r_k(j') < r_k(i)}      (row side, any i)
+// and r_k(i) <= r_k(j)  <=>  p_k(i) <= q_k(j)  (if r_k(i) > r_k(j), j itself
+// is counted by p but not by q).  Local ranks are < 2^12, so two columns fit
+// one 32-bit word as 16-bit fields with a guard bit: (q | 0x8000) - p keeps
+// bit 15 iff q >= p, and the halves never borrow from each other.  For a pair
+// of columns (s, 16 + s) of a 32-column word:
+//     g = AND_k ((Qpair_k | guards) - p_k * 0x10001) & 0x80008000
+//     acc = (acc >> 1) + g          (16 steps; no bit ever crosses a half)
+// leaves bit c of acc = "row i dominates column c" in natural order: per
+// column pair (m-1) IMAD-pipe subtractions, ceil((m-1)/2) LOP3 and one LEA --
+// about half the instructions of the per-column sign-bit funnel above.
+constexpr int SUPER = 2048;
+constexpr int SUPER_TILES = SUPER / TILE;
+
+// lsorted[(T*FD + k)*SUPER ..] = sorted r_{k+1} of super-tile T's columns (padding: ~0u);
+// qpk: per tile jt, words ((jw*16 + s)*FD + k): low half column 32jw+s, high half 32jw+16+s.
+template <int FD>
+__global__ void __launch_bounds__(256) k_local_ranks(const uint4 *__restrict__ rec, int64_t Np,
+                                                     uint32_t *__restrict__ lsorted,
+                                                     uint32_t *__restrict__ qpk) {
+    constexpr int NV = (FD + 1 + 3) / 4;
+    constexpr int IPT = SUPER / 256;
+    using Sort = cub::BlockRadixSort<uint32_t, 256, IPT>;
+    __shared__ typename Sort::TempStorage tmp;
+    __shared__ uint32_t srt[SUPER];
+    const int64_t T = blockIdx.x;
+    const int k = blockIdx.y;
+    const int tid = threadIdx.x;
+    uint32_t key[IPT], mine[IPT];
+#pragma unroll
+    for (int t = 0; t < IPT; ++t) {
+        const int64_t j = T * SUPER + tid * IPT + t;
+        key[t] = j < Np ? fld(rec + j * NV, k) : 0xFFFFFFFFu;
+        mine[t] = key[t];
+    }
+    Sort(tmp).Sort(key);
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < IPT; ++t) {
+        srt[tid * IPT + t] = key[t];
+        lsorted[((int64_t)T * FD + k) * SUPER + tid * IPT + t] = key[t];
+    }
+    __syncthreads();
+    uint16_t *q16 = reinterpret_cast<uint16_t *>(qpk);
+#pragma unroll
+    for (int t = 0; t < IPT; ++t) {
+        const int64_t j = T * SUPER + tid * IPT + t;
+        if (j >= Np) break;
+        const uint32_t v = mine[t];
+        int lo = 0;  // first position with srt[pos] >= v
+#pragma unroll
+        for (int step = SUPER / 2; step; step >>= 1)
+            if (srt[lo + step - 1] < v) lo += step;
+        const int64_t jt = j / TILE;
+        const int c = (int)(j % TILE), jw = c >> 5, cc = c & 31;
+        const int64_t word = jt * (TILE / 2) * FD + ((jw * 16 + (cc & 15)) * FD + k);
+        q16[2 * word + (cc >> 4)] = (uint16_t)(lo | 0x8000);
+    }
+}
+
+// lower bound count of v in a sorted SUPER-long array
+__device__ __forceinline__ uint32_t count_below(const uint32_t *__restrict__ srt, uint32_t v) {
+    int lo = 0;
+#pragma unroll
+    for (int step = SUPER / 2; step; step >>= 1)
+        if (__ldg(srt + lo + step - 1) < v) lo += step;
+    if (__ldg(srt + lo) < v) ++lo;  // only possible at lo == SUPER - 1
+    return (uint32_t)lo;
+}
+
+// super-row a (row tiles [8a, 8a+8)) x super-tiles [a, K): items before super-row a
+__device__ __forceinline__ int64_t packed_items_before(int64_t a, int64_t K) {
+    return SUPER_TILES * (a * K - a * (a - 1) / 2);
+}
+
+template <int M>
+__global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ rec,
+                                                     const uint32_t *__restrict__ qpk,
+                                                     const uint32_t *__restrict__ lsorted, int64_t N,
+                                                     int64_t nT, BitLayout L,
+                                                     uint32_t *__restrict__ bits,
+                                                     int32_t *__restrict__ cnt) {
+    constexpr int NV = (M + 3) / 4;
+    constexpr int FD = M - 1;
+    static_assert(FD >= 1, "packed K1 needs m >= 2");
+    __shared__ uint4 sJ[TILE * NV];
+    __shared__ __align__(16) uint32_t sQ[TILE / 2 * FD];
+    __shared__ uint32_t sB[TILE * 9];
+    __shared__ int32_t sCnt[TILE];
+    __shared__ int64_t s_it, s_T;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t K = (nT + SUPER_TILES - 1) / SUPER_TILES;
+    int64_t it, T;
+    if (!L.grid2d) {
+        if (tid == 0) {
+            const int64_t item = blockIdx.x;
+            int64_t lo = 0, hi = K - 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (packed_items_before(mid, K) <= item) lo = mid; else hi = mid - 1;
+            }
+            const int64_t local = item - packed_items_before(lo, K);
+            s_it = SUPER_TILES * lo + local / (K - lo);
+            s_T = lo + local % (K - lo);
+        }
+        __syncthreads();
+        it = s_it;
+        T = s_T;
+    } else {
+        it = blockIdx.y;
+        T = L.jt_lo / SUPER_TILES + blockIdx.x;
+    }
+    if (it >= nT) return;
+    int64_t jt0 = T * SUPER_TILES;
+    jt0 = max(jt0, max(it, L.jt_lo));
+    const int64_t jt1 = min((T + 1) * SUPER_TILES, L.jt_hi);
+    if (jt0 >= jt1) return;
+    const int64_t i = it * TILE + tid;
+    const bool row_ok = i < N;
+    uint32_t nf[4 * NV];  // general path: v + nf = r(j) - r(i) (id field: id(j) - id(i) - 1)
+    uint32_t P[FD];       // packed path: local rank of r_k(i), replicated in both halves
+    {
+        uint4 ri[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) ri[v] = rec[i * NV + v];
+#pragma unroll
+        for (int k = 0; k < 4 * NV; ++k) nf[k] = 0u - fld(ri, k);
+        nf[M - 1] -= 1u;
+#pragma unroll
+        for (int k = 0; k < FD; ++k)
+            P[k] = count_below(lsorted + (T * FD + k) * SUPER, fld(ri, k)) * 0x10001u;
+    }
+    const uint32_t last_i_id = fld(&rec[(it * TILE + TILE - 1) * NV], M - 1);
+    const Transpose32 transpose(lane);
+    const int64_t row_off = L.off[it], row_lo = L.lo_w[it], row_stride = L.stride[it];
+    for (int64_t jt = jt0; jt < jt1; ++jt) {
+        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sJ[tid * NV + v] = rec[(jt * TILE + tid) * NV + v];
+        for (int w = tid; w < TILE / 2 * FD; w += TILE) sQ[w] = qpk[jt * (TILE / 2) * FD + w];
+        sCnt[tid] = 0;
+        __syncthreads();
+        // run ids of the two tiles do not overlap -> no duplicate tuples across them
+        const bool disjoint = last_i_id < fld(&sJ[0], M - 1);
+        const int64_t tail = N - jt * TILE;  // columns past N are masked
+#pragma unroll 1
+        for (int jw = 0; jw < 8; ++jw) {
+            uint32_t word;
+            if (disjoint) {
+                uint32_t acc = 0;
+                if constexpr (FD == 2) {
+                    const uint4 *q4 = reinterpret_cast<const uint4 *>(sQ) + jw * 8;
+#pragma unroll
+                    for (int s2 = 0; s2 < 8; ++s2) {
+                        const uint4 v = q4[s2];
+                        acc = (acc >> 1) + ((v.x - P[0]) & (v.y - P[FD - 1]) & 0x80008000u);
+                        acc = (acc >> 1) + ((v.z - P[0]) & (v.w - P[FD - 1]) & 0x80008000u);
+                    }
+                } else {
+                    const uint32_t *q = sQ + jw * 16 * FD;
+#pragma unroll
+                    for (int s = 0; s < 16; ++s) {
+                        uint32_t g = 0x80008000u;
+#pragma unroll
+                        for (int k = 0; k < FD; ++k) g &= q[s * FD + k] - P[k];
+                        acc = (acc >> 1) + g;
+                    }
+                }
+                word = acc;
+            } else {
+                uint32_t acc = 0;
+#pragma unroll 8
+                for (int b = 0; b < 32; ++b) {
+                    const uint4 *v = &sJ[(jw * 32 + b) * NV];
+                    uint32_t x = fld(v, M - 1) + nf[M - 1];
+#pragma unroll
+                    for (int k = 0; k < M - 1; ++k) x |= fld(v, k) + nf[k];
+                    acc = __funnelshift_l(x, acc, 1);
+                }
+                word = __brev(~acc);
+            }
+            if (!row_ok) word = 0u;
+            const int64_t base = 32 * jw;
+            if (tail < base + 32) word &= tail <= base ? 0u : (1u << (tail - base)) - 1u;
+            sB[tid * 9 + jw] = word;
+            const int c = __popc(transpose(word));
+            if (c) atomicAdd(&sCnt[jw * 32 + lane], c);
+        }
+        __syncthreads();
+        if (row_ok) {
+            uint32_t *dst = bits + row_off + (int64_t)tid * row_stride + (8 * jt - row_lo);
+            const uint32_t *s = sB + tid * 9;
+            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(s[0], s[1], s[2], s[3]);
+            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(s[4], s[5], s[6], s[7]);
+        }
+        const int c = sCnt[tid];
+        if (c) atomicAdd(cnt + (jt - L.jt_lo) * TILE + tid, c);
+    }
+}
+
 // ------------------------------------------------------------------ K2
 struct PeelArgs {
     const uint32_t *bits;
@@ -629,6 +844,16 @@ __global__ void k_inverse(const int32_t *__restrict__ order, int64_t N, int32_t 
 }
 
 // ------------------------------------------------------------------ host
+// TEMO_K1_UNPACKED=1 selects the per-column sign-bit kernel (A/B comparisons)
+static bool packed_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_K1_UNPACKED");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 static inline dim3 grid1(int64_t n, int t = 256) { return dim3((unsigned)((n + t - 1) / t)); }
 
 // K0: column ranks, lex order (p.vals_a), run ids and records (p.rec)
@@ -674,9 +899,38 @@ static int build_records(RankPlan &p, const double *F, int32_t *status, cudaStre
 }
 
 // K1 over the column tiles of `L`; cnt (zeroed here) is indexed from column tile L.jt_lo
-static int launch_dom(int m, const uint4 *rec, int64_t N, int64_t nT, const BitLayout &L,
-                      uint32_t *bits, int32_t *cnt, cudaStream_t st) {
+static int launch_dom(const RankPlan &p, const BitLayout &L, uint32_t *bits, int32_t *cnt,
+                      cudaStream_t st) {
+    const int m = p.m;
+    const uint4 *rec = p.rec;
+    const int64_t N = p.N, nT = p.nT;
     stage_begin(S_DOM_BITS, st);
+    if (m >= 2 && !packed_disabled()) {
+        const int64_t K = (nT + SUPER_TILES - 1) / SUPER_TILES;
+        dim3 g;
+        if (L.grid2d) {
+            const int64_t T0 = L.jt_lo / SUPER_TILES, T1 = (L.jt_hi + SUPER_TILES - 1) / SUPER_TILES;
+            g = dim3((unsigned)(T1 - T0), (unsigned)L.jt_hi);
+        } else {
+            g = dim3((unsigned)(SUPER_TILES * (K * (K + 1) / 2)));
+        }
+        TEMO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * TILE * (L.jt_hi - L.jt_lo), st));
+#define PACK_CASE(MM)                                                                              \
+    case MM:                                                                                       \
+        k_local_ranks<MM - 1><<<dim3((unsigned)K, MM - 1), 256, 0, st>>>(rec, p.Np, p.lsorted, p.qpk); \
+        k_dom_packed<MM><<<g, TILE, 0, st>>>(rec, p.qpk, p.lsorted, N, nT, L, bits, cnt);           \
+        break;
+        switch (m) {
+            PACK_CASE(2) PACK_CASE(3) PACK_CASE(4) PACK_CASE(5) PACK_CASE(6) PACK_CASE(7) PACK_CASE(8)
+            PACK_CASE(9) PACK_CASE(10) PACK_CASE(11) PACK_CASE(12) PACK_CASE(13) PACK_CASE(14)
+            PACK_CASE(15) PACK_CASE(16)
+            default: return TEMO_EINVAL;
+        }
+#undef PACK_CASE
+        TEMO_LAUNCH_CHECK();
+        stage_end(S_DOM_BITS, st);
+        return TEMO_OK;
+    }
     dim3 g;
     if (L.grid2d) {
         g = dim3((unsigned)((L.jt_hi - L.jt_lo + CHUNK - 1) / CHUNK), (unsigned)L.jt_hi);
@@ -704,7 +958,7 @@ static int build_bitmap(RankPlan &p, const double *F, int32_t *status, cudaStrea
     if (rc) return rc;
     k_rowtile_offsets<<<grid1(p.nT), 256, 0, st>>>(p.nT, p.W, p.rt_off, p.rt_lo, p.rt_stride);
     BitLayout L{0, p.nT, p.rt_off, p.rt_lo, p.rt_stride, 0};
-    return launch_dom(p.m, p.rec, p.N, p.nT, L, p.bits, p.cnt, st);
+    return launch_dom(p, L, p.bits, p.cnt, st);
 }
 
 static int peel_grid(int NB, size_t smem) {

@@ -62,6 +62,7 @@ static void plan_shard(ShardPlan &s, void *base, int64_t N, int m, int64_t jt_lo
     p.scan_b = c.take<int32_t>(N);
     p.R = c.take<uint32_t>((size_t)N * 4 * p.NV);
     p.rec = c.take<uint4>((size_t)p.Np * p.NV);
+    take_packed(p, c);
     p.cub_tmp = c.take<char>(p.cub_bytes);
     s.off = c.take<int64_t>(p.nT + 1);
     s.lo = c.take<int64_t>(p.nT + 1);
@@ -302,7 +303,7 @@ extern "C" int temo_rank_shard_build(const double *F, int64_t N, int m, int64_t 
     const int64_t nT = s.k0.nT;
     k_shard_offsets<<<grid1(nT), 256, 0, st>>>(nT, jt_lo, jt_hi, s.off, s.lo, s.stride);
     BitLayout L{jt_lo, jt_hi, s.off, s.lo, s.stride, 1};
-    rc = launch_dom(m, s.k0.rec, N, nT, L, s.bits, s.cnt, st);
+    rc = launch_dom(s.k0, L, s.bits, s.cnt, st);
     if (rc) return rc;
     k_shard_init<<<grid1(s.k0.Np), 256, 0, st>>>(s.rank_s, N, s.k0.Np, s.scal);
     TEMO_LAUNCH_CHECK();

@@ -59,7 +59,7 @@ int main(int argc, char **argv) {
     cudaEventCreate(&a); cudaEventCreate(&b);
     for (int r = 0; r < reps; ++r) {
         cudaEventRecord(a, 0);
-        int rc = temo_offspring(&P, &V, X, idx, idx + h, h, &st, 0, O, FO, 0);
+        int rc = temo_offspring(&P, &V, X, (const int64_t *)idx, (const int64_t *)(idx + h), h, &st, 0, O, FO, 0);
         cudaEventRecord(b, 0);
         cudaEventSynchronize(b);
         float ms = 0;

@@ -31,6 +31,35 @@ def test_dominance_matrix_golden_small(cuda):
         assert np.array_equal(dominance_matrix(F), ond.dominance_matrix(F)), i
 
 
+def _np_dominance(F, block=512):
+    N = F.shape[0]
+    D = np.zeros((N, N), dtype=np.int64)
+    for a in range(0, N, block):
+        X = F[a:a + block, None, :]
+        D[a:a + block] = ((X <= F[None]).all(-1) & (X < F[None]).any(-1))
+    return D
+
+
+@pytest.mark.parametrize("N,m,kind", [(5000, 3, "u"), (4500, 4, "i"), (6145, 2, "i"), (4200, 3, "dup")])
+def test_dominance_matrix_multi_supertile(cuda, N, m, kind):
+    """The packed K1 (local ranks per 2048-column super-tile, two columns per
+    subtraction) against a blocked NumPy restatement of ndsort.py:37-43, across
+    several super-tiles, with ties and duplicate rows straddling tile borders."""
+    from paper_2503_20286_b200 import dominance_matrix
+
+    rng = np.random.default_rng(N * m)
+    if kind == "u":
+        F = rng.random((N, m))
+    elif kind == "i":
+        F = rng.integers(0, 9, size=(N, m)).astype(float)
+    else:  # many exact duplicate rows, plus -0.0 / +0.0
+        base = rng.random((N // 7, m))
+        F = base[rng.integers(0, len(base), N)]
+        F[rng.random(N) < 0.05, 0] = -0.0
+        F[rng.random(N) < 0.05, 1] = 0.0
+    assert np.array_equal(dominance_matrix(F), _np_dominance(F))
+
+
 # -- ports of the reference's own tests (test_ndsort.py) ---------------------
 def test_known_answers(cuda):
     from paper_2503_20286_b200 import dominance_matrix, rank_assign
@@ -86,7 +115,8 @@ def test_permutation_equivariance_and_contiguity(cuda):
 
 
 @pytest.mark.parametrize("N,m,kind", [(3000, 3, "u"), (5000, 2, "u"), (4097, 5, "i"), (2000, 10, "u"),
-                                      (1025, 16, "u"), (6000, 3, "dtlz2"), (257, 1, "i")])
+                                      (1025, 16, "u"), (6000, 3, "dtlz2"), (257, 1, "i"),
+                                      (10241, 3, "u"), (9000, 4, "i")])
 def test_rank_vs_oracle_mid(cuda, N, m, kind):
     from paper_2503_20286_b200 import rank_assign
 
