@@ -235,7 +235,8 @@ struct Transpose32 {
             const uint32_t lowmask = q == 0 ? 0x0000FFFFu : q == 1 ? 0x00FF00FFu : q == 2 ? 0x0F0F0F0Fu
                                    : q == 3 ? 0x33333333u : 0x55555555u;
             const bool top = (lane & s) == 0;
-            keep[q] = top ? lowmask : ~lowmask;
+            // opaque to the optimiser: keeps keep[] in registers (one LOP3 per stage)
+            asm("mov.b32 %0, %1;" : "=r"(keep[q]) : "r"(top ? lowmask : ~lowmask));
             rot[q] = top ? s : 32 - s;
         }
     }
@@ -244,7 +245,9 @@ struct Transpose32 {
         for (int q = 0; q < 5; ++q) {
             const uint32_t y = __shfl_xor_sync(~0u, x, 16 >> q);
             const uint32_t t = __funnelshift_l(y, y, rot[q]);  // rotate left
-            x = (x & keep[q]) | (t & ~keep[q]);
+            uint32_t r;  // (x & keep) | (t & ~keep)
+            asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(x), "r"(t), "r"(keep[q]));
+            x = r;
         }
         return x;
     }
@@ -489,7 +492,6 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
     static_assert(FD >= 1, "packed K1 needs m >= 2");
     __shared__ uint4 sJ[TILE * NV];
     __shared__ __align__(16) uint32_t sQ[TILE / 2 * FD];
-    __shared__ uint32_t sB[TILE * 9];
     __shared__ int32_t sCnt[TILE];
     __shared__ int64_t s_it, s_T;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -546,11 +548,10 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
         __syncthreads();
         // run ids of the two tiles do not overlap -> no duplicate tuples across them
         const bool disjoint = last_i_id < fld(&sJ[0], M - 1);
-        const int64_t tail = N - jt * TILE;  // columns past N are masked
-#pragma unroll 1
-        for (int jw = 0; jw < 8; ++jw) {
-            uint32_t word;
-            if (disjoint) {
+        uint32_t w[8];
+        if (disjoint) {
+#pragma unroll
+            for (int jw = 0; jw < 8; ++jw) {
                 uint32_t acc = 0;
                 if constexpr (FD == 2) {
                     const uint4 *q4 = reinterpret_cast<const uint4 *>(sQ) + jw * 8;
@@ -570,10 +571,13 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
                         acc = (acc >> 1) + g;
                     }
                 }
-                word = acc;
-            } else {
+                w[jw] = acc;
+            }
+        } else {
+#pragma unroll
+            for (int jw = 0; jw < 8; ++jw) {
                 uint32_t acc = 0;
-#pragma unroll 8
+#pragma unroll 4
                 for (int b = 0; b < 32; ++b) {
                     const uint4 *v = &sJ[(jw * 32 + b) * NV];
                     uint32_t x = fld(v, M - 1) + nf[M - 1];
@@ -581,22 +585,25 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
                     for (int k = 0; k < M - 1; ++k) x |= fld(v, k) + nf[k];
                     acc = __funnelshift_l(x, acc, 1);
                 }
-                word = __brev(~acc);
+                w[jw] = __brev(~acc);
             }
-            if (!row_ok) word = 0u;
-            const int64_t base = 32 * jw;
-            if (tail < base + 32) word &= tail <= base ? 0u : (1u << (tail - base)) - 1u;
-            sB[tid * 9 + jw] = word;
-            const int c = __popc(transpose(word));
-            if (c) atomicAdd(&sCnt[jw * 32 + lane], c);
+        }
+        const int64_t tail = N - jt * TILE;  // columns past N are masked
+#pragma unroll
+        for (int jw = 0; jw < 8; ++jw) {
+            if (!row_ok) w[jw] = 0u;
+            if (tail < TILE) {
+                const int64_t base = 32 * jw;
+                if (tail < base + 32) w[jw] &= tail <= base ? 0u : (1u << (tail - base)) - 1u;
+            }
+            atomicAdd(&sCnt[jw * 32 + lane], __popc(transpose(w[jw])));
+        }
+        if (row_ok) {
+            uint4 *dst = reinterpret_cast<uint4 *>(bits + row_off + (int64_t)tid * row_stride + (8 * jt - row_lo));
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
         }
         __syncthreads();
-        if (row_ok) {
-            uint32_t *dst = bits + row_off + (int64_t)tid * row_stride + (8 * jt - row_lo);
-            const uint32_t *s = sB + tid * 9;
-            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(s[0], s[1], s[2], s[3]);
-            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(s[4], s[5], s[6], s[7]);
-        }
         const int c = sCnt[tid];
         if (c) atomicAdd(cnt + (jt - L.jt_lo) * TILE + tid, c);
     }
