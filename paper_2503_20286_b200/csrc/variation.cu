@@ -306,6 +306,279 @@ __global__ void __launch_bounds__(VT, 6) k_offspring(temo_problem P, VarArgs V, 
     if (threadIdx.x < M) FO[(h + q) * M + threadIdx.x] = f[threadIdx.x];
 }
 
+// ------------------------------------------------- fused offspring, warp per pair
+// One warp owns a parent pair; lane t owns the Philox-aligned gene quad
+// [4t - sh, 4t - sh + 4) (+128 per round), so every stream's 4 uniforms are
+// exactly one Philox block (valid when h*d % 4 == 0, i.e. all streams are
+// congruent mod 4).  Straight-line per quad: 3 (SBX) + 2 (PM hit) blocks;
+// crossed/swap draws reduce to the raw word's top bit (U < 0.5 <=> raw < 2^63);
+// pow only on crossed genes (one call site per gene); PM only where hit.
+// Children go to O as they are made; the objective accumulation (LSMOP1 group
+// sums with x_1 broadcast from lane 0, or the DTLZ g sum) is a per-lane
+// partial reduced with warp shuffles -- no CTA barriers.
+constexpr int OW = 8;  // pairs (warps) per CTA
+
+// the 4 raw words of stream elements [e, e + 4) where (e - avail) % 4 == 0 (or e < avail)
+__device__ __forceinline__ void raw_quad(const Philox &ph, int64_t e, int64_t avail, uint64_t r[4]) {
+    if (e >= avail) {
+        uint64_t c[4];
+        ctr_add(ph.ctr, (uint64_t)((e - avail) >> 2) + 1, c);
+        philox_block(c, ph.key, r);
+    } else {  // head of the stream: buffered words of the host generator (negative e: masked genes)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t x = e + k;
+            r[k] = (x >= 0 && x < avail) ? ph.buf[ph.pos + x] : 0ull;
+        }
+    }
+}
+
+__device__ __forceinline__ double u01(uint64_t raw) {
+    return (double)(raw >> 11) * (1.0 / 9007199254740992.0);
+}
+
+template <int M>
+__device__ __forceinline__ void acc_gene(const temo_problem &P, int64_t g, double x, double x0,
+                                         double part[M]) {
+    if (P.id == TEMO_PROB_LSMOP1) {
+        const int64_t rel = g - (M - 1);
+        if (rel < 0 || rel >= P.offset[M]) return;
+        const double xs = (1.0 + (double)(g + 1) / (double)P.d) * x - 10.0 * x0;
+        const double sq = xs * xs;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+            if (rel >= P.offset[i] && rel < P.offset[i + 1]) part[i] += sq;
+        return;
+    }
+    if (g < M - 1) return;
+    switch (P.id) {
+        case 1:
+        case 3: {
+            const double z = x - 0.5;
+            part[0] += z * z - cos(20.0 * PI * z);
+            break;
+        }
+        case 2:
+        case 4:
+        case 5: {
+            const double z = x - 0.5;
+            part[0] += z * z;
+            break;
+        }
+        case 6: part[0] += pow(x, 0.1); break;
+        default: part[0] += x; break;
+    }
+}
+
+// objectives from the reduced sums (same formulas as eval_row); x = the child row
+template <int M>
+__device__ void finish_objs(const temo_problem &P, const double *x, const double part[M], double *f) {
+    if (P.id == TEMO_PROB_LSMOP1) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const double gi = part[i] / (double)P.sublen[i] / (double)P.nk;
+            double head = 1.0;
+            for (int k = 0; k < M - 1 - i; ++k) head = head * x[k];
+            const double tail = i == 0 ? 1.0 : 1.0 - x[M - 1 - i];
+            f[i] = (1.0 + gi) * head * tail;
+        }
+        return;
+    }
+    const int id = P.id;
+    const int64_t k = P.d - M + 1;
+    const double s = part[0];
+    double g;
+    if (id == 1 || id == 3) g = 100.0 * ((double)k + s);
+    else if (id == 7) g = 1.0 + 9.0 / (double)k * s;
+    else g = s;
+    if (id == 1) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            double p = 1.0;
+            for (int q = 0; q < M - 1 - i; ++q) p = p * x[q];
+            if (i) p = p * (1.0 - x[M - 1 - i]);
+            f[i] = 0.5 * (1.0 + g) * p;
+        }
+        return;
+    }
+    if (id == 7) {
+        double hsum = 0.0;
+        for (int q = 0; q < M - 1; ++q) {
+            f[q] = x[q];
+            hsum += x[q] / (1.0 + g) * (1.0 + sin(3.0 * PI * x[q]));
+        }
+        f[M - 1] = (1.0 + g) * ((double)M - hsum);
+        return;
+    }
+    double th[M];
+#pragma unroll
+    for (int q = 0; q < M - 1; ++q) {
+        if (id == 4) th[q] = pow(x[q], 100.0) * (PI / 2.0);
+        else if (id == 5 || id == 6) {
+            if (q == 0) th[q] = x[0] * (PI / 2.0);
+            else th[q] = PI / (4.0 * (1.0 + g)) * (1.0 + 2.0 * g * x[q]);
+        } else th[q] = x[q] * (PI / 2.0);
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double p = 1.0;
+        for (int q = 0; q < M - 1 - i; ++q) p = p * cos(th[q]);
+        if (i) p = p * sin(th[M - 1 - i]);
+        f[i] = (1.0 + g) * p;
+    }
+}
+
+__device__ __forceinline__ double pick4(const double v[4], int k) {
+    return k == 0 ? v[0] : k == 1 ? v[1] : k == 2 ? v[2] : v[3];
+}
+
+template <int M, bool SWAP>
+__global__ void __launch_bounds__(OW * 32, 2) k_offspring_w(temo_problem P, VarArgs V,
+                                                         const double *__restrict__ X,
+                                                         const int64_t *__restrict__ i1,
+                                                         const int64_t *__restrict__ i2, int64_t h,
+                                                         Philox ph, uint64_t off,
+                                                         double *__restrict__ O,
+                                                         double *__restrict__ FO, int single) {
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * OW + (threadIdx.x >> 5);
+    if (q >= h) return;
+    const int64_t d = P.d;
+    const double *x1 = X + i1[q] * d;
+    const double *x2 = X + i2[q] * d;
+    double *o1 = O + q * d;
+    double *o2 = O + (h + q) * d;
+    const int64_t hd = h * d;
+    const int64_t o_mu = (int64_t)off, o_swap = o_mu + hd, o_cross = o_mu + (SWAP ? 2 * hd : 0);
+    const int64_t o_pmu = o_mu + (SWAP ? 3 * hd : hd);
+    const int64_t o_hit = o_pmu + (single ? hd : 2 * hd);
+    const int64_t avail = 4 - ph.pos;
+    const double e = 1.0 / (V.eta_c + 1.0);
+    const double eta = V.eta_m + 1.0;
+    // gene 0 sits at lane position sh of its Philox block (same for every stream)
+    const int sh = (int)((o_mu + q * d - avail) & 3);
+    double part1[M], part2[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) part1[i] = part2[i] = 0.0;
+    double x0a = 0.0, x0b = 0.0;
+    for (int64_t base = -sh; base < d; base += 128) {
+        const int64_t gs = base + 4 * lane;
+        const int64_t es = q * d + gs;  // stream element of gene gs (child 1 / pair index)
+        double a[4], b[4], c1[4], c2[4];
+        bool ok[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t g = gs + k;
+            ok[k] = g >= 0 && g < d;
+            a[k] = ok[k] ? __ldg(x1 + g) : 0.0;
+            b[k] = ok[k] ? __ldg(x2 + g) : 0.0;
+        }
+        // --- SBX (variation.py:72-91)
+        uint32_t crossed = 0xF, negate = 0;
+        if (SWAP) {
+            uint64_t r[4];
+            raw_quad(ph, o_cross + es, avail, r);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) crossed &= ~((uint32_t)(r[k] >> 63) << k);  // U < 0.5 <=> top bit 0
+            raw_quad(ph, o_swap + es, avail, r);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) negate |= (uint32_t)(1u - (uint32_t)(r[k] >> 63)) << k;
+        }
+        {
+            uint64_t r[4];
+            raw_quad(ph, o_mu + es, avail, r);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t g = gs + k;
+                double y1 = a[k], y2 = b[k];
+                if ((crossed >> k) & 1) {
+                    const double mu = u01(r[k]);
+                    const double base_ = (0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu);
+                    double beta = pow(base_, e);
+                    if (SWAP) beta = beta * (1.0 - 2.0 * (double)((negate >> k) & 1));
+                    const double shift = 0.5 * (1.0 - beta);
+                    y1 = a[k] + shift * (b[k] - a[k]);
+                    y2 = b[k] + shift * (a[k] - b[k]);
+                }
+                if (ok[k]) {
+                    const double lo = __ldg(V.lower + g), hi = __ldg(V.upper + g);
+                    y1 = clipv(y1, lo, hi);
+                    y2 = clipv(y2, lo, hi);
+                }
+                c1[k] = y1;
+                c2[k] = y2;
+            }
+        }
+        // --- polynomial mutation (variation.py:104-120), only where hit
+        {
+            uint64_t r[4];
+            raw_quad(ph, o_hit + es, avail, r);
+            uint32_t hit = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) hit |= (uint32_t)(ok[k] && V.p_m - u01(r[k]) >= 0.0) << k;
+            if (!single) {
+                raw_quad(ph, o_hit + hd + es, avail, r);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) hit |= (uint32_t)(ok[k] && V.p_m - u01(r[k]) >= 0.0) << (4 + k);
+            }
+            if (hit) {
+                uint64_t m1[4], m2[4];
+                if (hit & 0xF) raw_quad(ph, o_pmu + es, avail, m1);
+                if (hit & 0xF0) raw_quad(ph, o_pmu + hd + es, avail, m2);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t g = gs + k;
+                    if ((hit >> k) & 1) {
+                        const double lo = V.lower[g], hi = V.upper[g];
+                        c1[k] = clipv(pm_step(c1[k], lo, hi, u01(m1[k]), eta), lo, hi);
+                    }
+                    if ((hit >> (4 + k)) & 1) {
+                        const double lo = V.lower[g], hi = V.upper[g];
+                        c2[k] = clipv(pm_step(c2[k], lo, hi, u01(m2[k]), eta), lo, hi);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (ok[k]) {
+                o1[gs + k] = c1[k];
+                if (!single) o2[gs + k] = c2[k];
+            }
+        if (!FO) continue;
+        if (base == -sh) {  // first round: lane 0 holds gene 0 at quad position sh
+            x0a = __shfl_sync(~0u, pick4(c1, sh), 0);
+            x0b = __shfl_sync(~0u, pick4(c2, sh), 0);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (ok[k]) {
+                acc_gene<M>(P, gs + k, c1[k], x0a, part1);
+                if (!single) acc_gene<M>(P, gs + k, c2[k], x0b, part2);
+            }
+    }
+    if (!FO) return;
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int s = 16; s; s >>= 1) {
+            part1[i] += __shfl_xor_sync(~0u, part1[i], s);
+            part2[i] += __shfl_xor_sync(~0u, part2[i], s);
+        }
+    __syncwarp();
+    if (lane == 0) {
+        double f[M];
+        finish_objs<M>(P, o1, part1, f);
+#pragma unroll
+        for (int i = 0; i < M; ++i) FO[q * M + i] = f[i];
+    } else if (lane == 1 && !single) {
+        double f[M];
+        finish_objs<M>(P, o2, part2, f);
+#pragma unroll
+        for (int i = 0; i < M; ++i) FO[(h + q) * M + i] = f[i];
+    }
+}
+
 // ------------------------------------------------------------------ standalone operators
 __global__ void k_sbx(VarArgs V, const double *__restrict__ X1, const double *__restrict__ X2,
                       int64_t q, int64_t d, Philox ph, USrc umu, USrc usw, USrc ucr,
@@ -357,6 +630,16 @@ __global__ void k_init_population(Philox ph, uint64_t off, int64_t rows, int64_t
         const int64_t g = t % d;
         X[t] = lo[g] + c.uniform(ph, off + t) * (hi[g] - lo[g]);
     }
+}
+
+// TEMO_OFFSPRING_CTA=1 selects the CTA-per-pair kernel (A/B comparisons)
+static bool offspring_cta_forced() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_OFFSPRING_CTA");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
 }
 
 static VarArgs var_args(const temo_variation *v) {
@@ -459,14 +742,24 @@ static int launch_offspring(const temo_problem *prob, const temo_variation *var,
     const int64_t d = prob->d;
     const int smem_rows = 2 * d * (int64_t)sizeof(double) <= 96 * 1024;
     const size_t smem = smem_rows ? 2 * d * sizeof(double) : 0;
+    // warp-per-pair kernel whenever every stream is congruent mod 4 (one Philox block per quad)
+    const bool warp_path = (h * d) % 4 == 0 && !offspring_cta_forced();
     stage_begin(S_OFFSPRING, s);
 #define OFF_CASE(MM)                                                                              \
     case MM:                                                                                      \
-        if (smem > 48 * 1024)                                                                     \
-            TEMO_CUDA(cudaFuncSetAttribute(k_offspring<MM>,                                       \
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)); \
-        k_offspring<MM><<<(unsigned)h, VT, smem, s>>>(*prob, var_args(var), X, i1, i2, h,         \
-                                                      philox_from(*st), off, O, FO, smem_rows, single); \
+        if (warp_path && var->gene_swap)                                                          \
+            k_offspring_w<MM, true><<<(unsigned)((h + OW - 1) / OW), OW * 32, 0, s>>>(            \
+                *prob, var_args(var), X, i1, i2, h, philox_from(*st), off, O, FO, single);        \
+        else if (warp_path)                                                                       \
+            k_offspring_w<MM, false><<<(unsigned)((h + OW - 1) / OW), OW * 32, 0, s>>>(           \
+                *prob, var_args(var), X, i1, i2, h, philox_from(*st), off, O, FO, single);        \
+        else {                                                                                    \
+            if (smem > 48 * 1024)                                                                 \
+                TEMO_CUDA(cudaFuncSetAttribute(k_offspring<MM>,                                   \
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)); \
+            k_offspring<MM><<<(unsigned)h, VT, smem, s>>>(*prob, var_args(var), X, i1, i2, h,     \
+                                                          philox_from(*st), off, O, FO, smem_rows, single); \
+        }                                                                                         \
         break;
     TEMO_M_SWITCH(prob->m, OFF_CASE)
 #undef OFF_CASE
