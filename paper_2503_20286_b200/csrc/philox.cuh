@@ -33,8 +33,13 @@ __device__ __forceinline__ void philox_block(const uint64_t ctr_in[4], const uin
                                              uint64_t out[4]) {
     uint64_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
     uint64_t k0 = key_in[0], k1 = key_in[1];
+#ifdef OFF_ABL_PHILOX
+#pragma unroll
+    for (int r = 0; r < 1; ++r) {
+#else
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
+#endif
         if (r) {
             k0 += 0x9E3779B97F4A7C15ull;
             k1 += 0xBB67AE8584CAA73Bull;
@@ -48,6 +53,39 @@ __device__ __forceinline__ void philox_block(const uint64_t ctr_in[4], const uin
         c3 = lo0;
     }
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+// NB independent blocks in lockstep (ILP across the serial 10-round chains)
+template <int NB>
+__device__ __forceinline__ void philox_blocks(const uint64_t ctr[NB][4], const uint64_t key_in[2],
+                                              uint64_t out[NB][4]) {
+    uint64_t c0[NB], c1[NB], c2[NB], c3[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        c0[b] = ctr[b][0]; c1[b] = ctr[b][1]; c2[b] = ctr[b][2]; c3[b] = ctr[b][3];
+    }
+    uint64_t k0 = key_in[0], k1 = key_in[1];
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B97F4A7C15ull;
+            k1 += 0xBB67AE8584CAA73Bull;
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const uint64_t lo0 = 0xD2E7470EE14C6C93ull * c0[b], hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c0[b]);
+            const uint64_t lo1 = 0xCA5A826395121157ull * c2[b], hi1 = __umul64hi(0xCA5A826395121157ull, c2[b]);
+            const uint64_t n0 = hi1 ^ c1[b] ^ k0, n2 = hi0 ^ c3[b] ^ k1;
+            c0[b] = n0;
+            c1[b] = lo1;
+            c2[b] = n2;
+            c3[b] = lo0;
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        out[b][0] = c0[b]; out[b][1] = c1[b]; out[b][2] = c2[b]; out[b][3] = c3[b];
+    }
 }
 
 // counter + add (256-bit, little-endian words)

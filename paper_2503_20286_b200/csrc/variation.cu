@@ -316,7 +316,22 @@ __global__ void __launch_bounds__(VT, 6) k_offspring(temo_problem P, VarArgs V, 
 // Children go to O as they are made; the objective accumulation (LSMOP1 group
 // sums with x_1 broadcast from lane 0, or the DTLZ g sum) is a per-lane
 // partial reduced with warp shuffles -- no CTA barriers.
-constexpr int OW = 8;  // pairs (warps) per CTA
+#ifndef OFF_LOCKSTEP
+#define OFF_LOCKSTEP 1
+#endif
+#ifndef OFF_EXPLOG
+#define OFF_EXPLOG 0
+#endif
+#ifndef OFF_ACC_QUAD
+#define OFF_ACC_QUAD 0
+#endif
+#ifndef OFF_OW
+#define OFF_OW 8
+#endif
+#ifndef OFF_MINB
+#define OFF_MINB 2
+#endif
+constexpr int OW = OFF_OW;  // pairs (warps) per CTA
 
 // the 4 raw words of stream elements [e, e + 4) where (e - avail) % 4 == 0 (or e < avail)
 __device__ __forceinline__ void raw_quad(const Philox &ph, int64_t e, int64_t avail, uint64_t r[4]) {
@@ -330,6 +345,24 @@ __device__ __forceinline__ void raw_quad(const Philox &ph, int64_t e, int64_t av
             const int64_t x = e + k;
             r[k] = (x >= 0 && x < avail) ? ph.buf[ph.pos + x] : 0ull;
         }
+    }
+}
+
+// raw words of NS streams at elements E[s] (each aligned as in raw_quad), blocks in lockstep
+template <int NS>
+__device__ __forceinline__ void raw_quads(const Philox &ph, const int64_t E[NS], int64_t avail,
+                                          uint64_t r[NS][4]) {
+    bool head = false;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) head |= E[s] < avail;
+    if (!head) {
+        uint64_t c[NS][4];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) ctr_add(ph.ctr, (uint64_t)((E[s] - avail) >> 2) + 1, c[s]);
+        philox_blocks<NS>(c, ph.key, r);
+    } else {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) raw_quad(ph, E[s], avail, r[s]);
     }
 }
 
@@ -368,6 +401,35 @@ __device__ __forceinline__ void acc_gene(const temo_problem &P, int64_t g, doubl
         case 6: part[0] += pow(x, 0.1); break;
         default: part[0] += x; break;
     }
+}
+
+// four consecutive genes [g, g+4) of one child; one group lookup when the quad lies in one group
+template <int M>
+__device__ __forceinline__ void acc_quad(const temo_problem &P, int64_t g, const double x[4],
+                                         const bool ok[4], bool full, double x0, double part[M]) {
+    if (P.id == TEMO_PROB_LSMOP1 && full) {
+        const int64_t rel = g - (M - 1);
+        int grp = -1;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+            if (rel >= P.offset[i] && rel + 3 < P.offset[i + 1]) grp = i;
+        if (grp >= 0) {
+            const double inv_d = 1.0 / (double)P.d;
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double xs = (1.0 + (double)(g + k + 1) * inv_d) * x[k] - 10.0 * x0;
+                s += xs * xs;
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                if (i == grp) part[i] += s;
+            return;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (ok[k]) acc_gene<M>(P, g + k, x[k], x0, part);
 }
 
 // objectives from the reduced sums (same formulas as eval_row); x = the child row
@@ -433,7 +495,7 @@ __device__ __forceinline__ double pick4(const double v[4], int k) {
 }
 
 template <int M, bool SWAP>
-__global__ void __launch_bounds__(OW * 32, 2) k_offspring_w(temo_problem P, VarArgs V,
+__global__ void __launch_bounds__(OW * 32, OFF_MINB) k_offspring_w(temo_problem P, VarArgs V,
                                                          const double *__restrict__ X,
                                                          const int64_t *__restrict__ i1,
                                                          const int64_t *__restrict__ i2, int64_t h,
@@ -464,6 +526,38 @@ __global__ void __launch_bounds__(OW * 32, 2) k_offspring_w(temo_problem P, VarA
     for (int64_t base = -sh; base < d; base += 128) {
         const int64_t gs = base + 4 * lane;
         const int64_t es = q * d + gs;  // stream element of gene gs (child 1 / pair index)
+        // --- the quad's uniform streams, Philox blocks in lockstep groups:
+        //     [cross, swap,] mu  then  hit c1, hit c2
+        constexpr int NS = SWAP ? 5 : 3;
+        uint64_t R[NS][4];
+        {
+            constexpr int NA = NS - 2;
+            int64_t E[NA];
+            if (SWAP) {
+                E[0] = o_cross + es;
+                E[1] = o_swap + es;
+            }
+            E[NA - 1] = o_mu + es;
+            const int64_t EH[2] = {o_hit + es, o_hit + hd + es};  // (second unused in single mode)
+#if OFF_LOCKSTEP == 2
+            {
+                int64_t EA[NS];
+#pragma unroll
+                for (int t = 0; t < NA; ++t) EA[t] = E[t];
+                EA[NA] = EH[0];
+                EA[NA + 1] = EH[1];
+                raw_quads<NS>(ph, EA, avail, R);
+            }
+#elif OFF_LOCKSTEP
+            raw_quads<NA>(ph, E, avail, R);
+            raw_quads<2>(ph, EH, avail, R + NA);
+#else
+#pragma unroll
+            for (int t = 0; t < NA; ++t) raw_quad(ph, E[t], avail, R[t]);
+            raw_quad(ph, EH[0], avail, R[NA]);
+            raw_quad(ph, EH[1], avail, R[NA + 1]);
+#endif
+        }
         double a[4], b[4], c1[4], c2[4];
         bool ok[4];
 #pragma unroll
@@ -476,50 +570,47 @@ __global__ void __launch_bounds__(OW * 32, 2) k_offspring_w(temo_problem P, VarA
         // --- SBX (variation.py:72-91)
         uint32_t crossed = 0xF, negate = 0;
         if (SWAP) {
-            uint64_t r[4];
-            raw_quad(ph, o_cross + es, avail, r);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) crossed &= ~((uint32_t)(r[k] >> 63) << k);  // U < 0.5 <=> top bit 0
-            raw_quad(ph, o_swap + es, avail, r);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) negate |= (uint32_t)(1u - (uint32_t)(r[k] >> 63)) << k;
-        }
-        {
-            uint64_t r[4];
-            raw_quad(ph, o_mu + es, avail, r);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const int64_t g = gs + k;
-                double y1 = a[k], y2 = b[k];
-                if ((crossed >> k) & 1) {
-                    const double mu = u01(r[k]);
-                    const double base_ = (0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu);
-                    double beta = pow(base_, e);
-                    if (SWAP) beta = beta * (1.0 - 2.0 * (double)((negate >> k) & 1));
-                    const double shift = 0.5 * (1.0 - beta);
-                    y1 = a[k] + shift * (b[k] - a[k]);
-                    y2 = b[k] + shift * (a[k] - b[k]);
-                }
-                if (ok[k]) {
-                    const double lo = __ldg(V.lower + g), hi = __ldg(V.upper + g);
-                    y1 = clipv(y1, lo, hi);
-                    y2 = clipv(y2, lo, hi);
-                }
-                c1[k] = y1;
-                c2[k] = y2;
+                crossed &= ~((uint32_t)(R[0][k] >> 63) << k);  // U < 0.5 <=> top bit 0
+                negate |= (uint32_t)(1u - (uint32_t)(R[1][k] >> 63)) << k;
             }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t g = gs + k;
+            double y1 = a[k], y2 = b[k];
+            if ((crossed >> k) & 1) {
+                // pow(2 mu, e) or pow(1 / (2 - 2 mu), e) as exp(+-e log(.)): e = 1/(eta_c+1) is
+                // small, so plain double log/exp keep ~1 ulp (children agree to rtol 1e-13)
+                const double mu = u01(R[NS - 3][k]);
+#if OFF_EXPLOG
+                const double beta0 = (0.5 - mu >= 0.0) ? exp(e * log(2.0 * mu)) : exp(-e * log(2.0 - 2.0 * mu));
+#elif OFF_ABL_POW
+                const double beta0 = (0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu);
+#else
+                const double beta0 = pow((0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu), e);
+#endif
+                const double beta = SWAP ? beta0 * (1.0 - 2.0 * (double)((negate >> k) & 1)) : beta0;
+                const double shift = 0.5 * (1.0 - beta);
+                y1 = a[k] + shift * (b[k] - a[k]);
+                y2 = b[k] + shift * (a[k] - b[k]);
+            }
+            if (ok[k]) {
+                const double lo = __ldg(V.lower + g), hi = __ldg(V.upper + g);
+                y1 = clipv(y1, lo, hi);
+                y2 = clipv(y2, lo, hi);
+            }
+            c1[k] = y1;
+            c2[k] = y2;
         }
         // --- polynomial mutation (variation.py:104-120), only where hit
         {
-            uint64_t r[4];
-            raw_quad(ph, o_hit + es, avail, r);
             uint32_t hit = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) hit |= (uint32_t)(ok[k] && V.p_m - u01(r[k]) >= 0.0) << k;
-            if (!single) {
-                raw_quad(ph, o_hit + hd + es, avail, r);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) hit |= (uint32_t)(ok[k] && V.p_m - u01(r[k]) >= 0.0) << (4 + k);
+            for (int k = 0; k < 4; ++k) {
+                hit |= (uint32_t)(ok[k] && V.p_m - u01(R[NS - 2][k]) >= 0.0) << k;
+                if (!single) hit |= (uint32_t)(ok[k] && V.p_m - u01(R[NS - 1][k]) >= 0.0) << (4 + k);
             }
             if (hit) {
                 uint64_t m1[4], m2[4];
@@ -550,12 +641,21 @@ __global__ void __launch_bounds__(OW * 32, 2) k_offspring_w(temo_problem P, VarA
             x0a = __shfl_sync(~0u, pick4(c1, sh), 0);
             x0b = __shfl_sync(~0u, pick4(c2, sh), 0);
         }
+        const bool full = gs >= 0 && gs + 4 <= d;
+#if OFF_ABL_EVAL
+        (void)full;
+#elif OFF_ACC_QUAD
+        acc_quad<M>(P, gs, c1, ok, full, x0a, part1);
+        if (!single) acc_quad<M>(P, gs, c2, ok, full, x0b, part2);
+#else
+        (void)full;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (ok[k]) {
                 acc_gene<M>(P, gs + k, c1[k], x0a, part1);
                 if (!single) acc_gene<M>(P, gs + k, c2[k], x0b, part2);
             }
+#endif
     }
     if (!FO) return;
 #pragma unroll
@@ -576,6 +676,225 @@ __global__ void __launch_bounds__(OW * 32, 2) k_offspring_w(temo_problem P, VarA
         finish_objs<M>(P, o2, part2, f);
 #pragma unroll
         for (int i = 0; i < M; ++i) FO[(h + q) * M + i] = f[i];
+    }
+}
+
+// -------------------------------------- fused offspring, persistent warps
+// k_offspring_s: the warp-per-pair scheme above, with
+//   - per-gene constants (bounds, LSMOP linkage coefficient 1 + g/d and
+//     group id) staged once per CTA in shared memory -- no per-gene DDIV;
+//   - persistent warps looping over pairs (the staging is amortised);
+//   - Philox blocks in two lockstep groups ([cross, swap,] mu | hit1, hit2);
+//   - SBX pows compacted across the warp: only crossed genes (about half)
+//     are queued in shared memory and every lane takes queue slots, so a
+//     warp round issues ceil(#crossed/32) pows instead of 4.
+constexpr int SW = 8;            // warps per CTA
+constexpr int SMAX_D = 3000;     // genes staged in shared memory (else k_offspring_w)
+
+template <int M, bool SWAP>
+__global__ void __launch_bounds__(SW * 32, 2) k_offspring_s(temo_problem P, VarArgs V,
+                                                            const double *__restrict__ X,
+                                                            const int64_t *__restrict__ i1,
+                                                            const int64_t *__restrict__ i2, int64_t h,
+                                                            Philox ph, uint64_t off,
+                                                            double *__restrict__ O,
+                                                            double *__restrict__ FO, int single) {
+    extern __shared__ double ssm[];
+    const int64_t d = P.d;
+    double *s_lo = ssm, *s_hi = ssm + d, *s_cf = ssm + 2 * d;
+    double *s_q = ssm + 3 * d + (threadIdx.x >> 5) * 128;  // per-warp pow queue
+    signed char *s_grp = reinterpret_cast<signed char *>(ssm + 3 * d + SW * 128);
+    const bool lsmop = P.id == TEMO_PROB_LSMOP1;
+    for (int64_t g = threadIdx.x; g < d; g += blockDim.x) {
+        s_lo[g] = V.lower[g];
+        s_hi[g] = V.upper[g];
+        s_cf[g] = 1.0 + (double)(g + 1) / (double)d;
+        int grp = -1;
+        const int64_t rel = g - (M - 1);
+        if (lsmop) {
+            for (int i = 0; i < M; ++i)
+                if (rel >= P.offset[i] && rel < P.offset[i + 1]) grp = i;
+        } else if (rel >= 0) {
+            grp = 0;
+        }
+        s_grp[g] = (signed char)grp;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t hd = h * d;
+    const int64_t o_mu = (int64_t)off, o_swap = o_mu + hd, o_cross = o_mu + (SWAP ? 2 * hd : 0);
+    const int64_t o_pmu = o_mu + (SWAP ? 3 * hd : hd);
+    const int64_t o_hit = o_pmu + (single ? hd : 2 * hd);
+    const int64_t avail = 4 - ph.pos;
+    const double e = 1.0 / (V.eta_c + 1.0);
+    const double eta = V.eta_m + 1.0;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int64_t q = (int64_t)blockIdx.x * SW + (threadIdx.x >> 5); q < h; q += (int64_t)gridDim.x * SW) {
+        const double *x1 = X + i1[q] * d;
+        const double *x2 = X + i2[q] * d;
+        double *o1 = O + q * d;
+        double *o2 = O + (h + q) * d;
+        const int sh = (int)((o_mu + q * d - avail) & 3);
+        double part1[M], part2[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) part1[i] = part2[i] = 0.0;
+        double x0a = 0.0, x0b = 0.0;
+        for (int64_t base = -sh; base < d; base += 128) {
+            const int64_t gs = base + 4 * lane;
+            const int64_t es = q * d + gs;
+            constexpr int NS = SWAP ? 5 : 3;
+            constexpr int NA = NS - 2;
+            uint64_t R[NS][4];
+            {
+                int64_t E[NA];
+                if (SWAP) {
+                    E[0] = o_cross + es;
+                    E[1] = o_swap + es;
+                }
+                E[NA - 1] = o_mu + es;
+                raw_quads<NA>(ph, E, avail, R);
+                const int64_t EH[2] = {o_hit + es, o_hit + hd + es};  // (second unused in single mode)
+                raw_quads<2>(ph, EH, avail, R + NA);
+            }
+            double a[4], b[4], c1[4], c2[4];
+            bool ok[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t g = gs + k;
+                ok[k] = g >= 0 && g < d;
+                a[k] = ok[k] ? __ldg(x1 + g) : 0.0;
+                b[k] = ok[k] ? __ldg(x2 + g) : 0.0;
+            }
+            // --- SBX (variation.py:72-91): crossed / swap are top-bit tests of the raw words
+            uint32_t crossed = 0xF, negate = 0;
+            if (SWAP) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    crossed &= ~((uint32_t)(R[0][k] >> 63) << k);
+                    negate |= (uint32_t)(1u - (uint32_t)(R[1][k] >> 63)) << k;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) crossed &= (uint32_t)ok[k] << k | ~(1u << k);
+            // queue the crossed genes' mu, pow them warp-wide, read the betas back
+            const int nq = __popc(crossed);
+            int incl = nq;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(~0u, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(~0u, incl, 31);
+            int slot = incl - nq;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if ((crossed >> k) & 1) s_q[slot++] = u01(R[NA - 1][k]);
+            __syncwarp();
+            for (int t = lane; t < total; t += 32) {
+                const double mu = s_q[t];
+                s_q[t] = pow((0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu), e);
+            }
+            __syncwarp();
+            slot = incl - nq;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t g = gs + k;
+                double y1 = a[k], y2 = b[k];
+                if ((crossed >> k) & 1) {
+                    const double beta0 = s_q[slot++];
+                    const double beta = SWAP ? beta0 * (1.0 - 2.0 * (double)((negate >> k) & 1)) : beta0;
+                    const double shift = 0.5 * (1.0 - beta);
+                    y1 = a[k] + shift * (b[k] - a[k]);
+                    y2 = b[k] + shift * (a[k] - b[k]);
+                }
+                if (ok[k]) {
+                    const double lo = s_lo[g], hi = s_hi[g];
+                    y1 = clipv(y1, lo, hi);
+                    y2 = clipv(y2, lo, hi);
+                }
+                c1[k] = y1;
+                c2[k] = y2;
+            }
+            __syncwarp();  // s_q reused next round
+            (void)lt_mask;
+            // --- polynomial mutation (variation.py:104-120), only where hit
+            uint32_t hit = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                hit |= (uint32_t)(ok[k] && V.p_m - u01(R[NS - 2][k]) >= 0.0) << k;
+                if (!single) hit |= (uint32_t)(ok[k] && V.p_m - u01(R[NS - 1][k]) >= 0.0) << (4 + k);
+            }
+            if (hit) {
+                uint64_t m1[4], m2[4];
+                if (hit & 0xF) raw_quad(ph, o_pmu + es, avail, m1);
+                if (hit & 0xF0) raw_quad(ph, o_pmu + hd + es, avail, m2);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t g = gs + k;
+                    if ((hit >> k) & 1)
+                        c1[k] = clipv(pm_step(c1[k], s_lo[g], s_hi[g], u01(m1[k]), eta), s_lo[g], s_hi[g]);
+                    if ((hit >> (4 + k)) & 1)
+                        c2[k] = clipv(pm_step(c2[k], s_lo[g], s_hi[g], u01(m2[k]), eta), s_lo[g], s_hi[g]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (ok[k]) {
+                    o1[gs + k] = c1[k];
+                    if (!single) o2[gs + k] = c2[k];
+                }
+            if (!FO) continue;
+            if (base == -sh) {  // lane 0 holds gene 0 at quad position sh
+                x0a = __shfl_sync(~0u, pick4(c1, sh), 0);
+                x0b = __shfl_sync(~0u, pick4(c2, sh), 0);
+            }
+            if (lsmop) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int grp = ok[k] ? (int)s_grp[gs + k] : -1;
+                    if (grp < 0) continue;
+                    const double cf = s_cf[gs + k];
+                    const double xa = cf * c1[k] - 10.0 * x0a;
+                    const double sa = xa * xa;
+                    const double xb = cf * c2[k] - 10.0 * x0b;
+                    const double sb = xb * xb;
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        if (grp == i) {
+                            part1[i] += sa;
+                            if (!single) part2[i] += sb;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (ok[k]) {
+                        acc_gene<M>(P, gs + k, c1[k], x0a, part1);
+                        if (!single) acc_gene<M>(P, gs + k, c2[k], x0b, part2);
+                    }
+            }
+        }
+        if (!FO) continue;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int s = 16; s; s >>= 1) {
+                part1[i] += __shfl_xor_sync(~0u, part1[i], s);
+                part2[i] += __shfl_xor_sync(~0u, part2[i], s);
+            }
+        __syncwarp();
+        if (lane == 0) {
+            double f[M];
+            finish_objs<M>(P, o1, part1, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[q * M + i] = f[i];
+        } else if (lane == 1 && !single) {
+            double f[M];
+            finish_objs<M>(P, o2, part2, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[(h + q) * M + i] = f[i];
+        }
     }
 }
 
@@ -630,6 +949,16 @@ __global__ void k_init_population(Philox ph, uint64_t off, int64_t rows, int64_t
         const int64_t g = t % d;
         X[t] = lo[g] + c.uniform(ph, off + t) * (hi[g] - lo[g]);
     }
+}
+
+// TEMO_OFFSPRING_S=0 disables the persistent staged kernel (A/B comparisons)
+static bool offspring_s_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_OFFSPRING_S");
+        v = (e && e[0] == '0') ? 1 : 0;
+    }
+    return v == 1;
 }
 
 // TEMO_OFFSPRING_CTA=1 selects the CTA-per-pair kernel (A/B comparisons)
@@ -747,7 +1076,23 @@ static int launch_offspring(const temo_problem *prob, const temo_variation *var,
     stage_begin(S_OFFSPRING, s);
 #define OFF_CASE(MM)                                                                              \
     case MM:                                                                                      \
-        if (warp_path && var->gene_swap)                                                          \
+        if (warp_path && d <= SMAX_D && !offspring_s_disabled()) {                                \
+            const size_t sm_s = (3 * d + SW * 128) * sizeof(double) + d + 16;                    \
+            if (sm_s > 48 * 1024) {                                                               \
+                TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<MM, true>,                          \
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s)); \
+                TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<MM, false>,                         \
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s)); \
+            }                                                                                     \
+            const int64_t want = (h + SW - 1) / SW;                                               \
+            const unsigned grid = (unsigned)(want < num_sms() * 2 * 4 ? want : num_sms() * 2 * 4);\
+            if (var->gene_swap)                                                                   \
+                k_offspring_s<MM, true><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h, \
+                                                                   philox_from(*st), off, O, FO, single); \
+            else                                                                                  \
+                k_offspring_s<MM, false><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h, \
+                                                                    philox_from(*st), off, O, FO, single); \
+        } else if (warp_path && var->gene_swap)                                                   \
             k_offspring_w<MM, true><<<(unsigned)((h + OW - 1) / OW), OW * 32, 0, s>>>(            \
                 *prob, var_args(var), X, i1, i2, h, philox_from(*st), off, O, FO, single);        \
         else if (warp_path)                                                                       \
