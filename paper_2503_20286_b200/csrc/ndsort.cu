@@ -480,6 +480,29 @@ __device__ __forceinline__ int64_t packed_items_before(int64_t a, int64_t K) {
     return SUPER_TILES * (a * K - a * (a - 1) / 2);
 }
 
+// 8 independent 32x32 transposes interleaved stage by stage (SHFL latency hidden)
+__device__ __forceinline__ void transpose8(const Transpose32 &t, uint32_t x[8]) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        uint32_t y[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) y[k] = __shfl_xor_sync(~0u, x[k], 16 >> q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t r = __funnelshift_l(y[k], y[k], t.rot[q]);
+            uint32_t o;
+            asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(o) : "r"(x[k]), "r"(r), "r"(t.keep[q]));
+            x[k] = o;
+        }
+    }
+}
+
+// Dynamic shared memory of k_dom_packed: sQ (all tiles of the item), sCnt, sJ (one tile)
+__host__ __device__ constexpr size_t packed_smem(int M) {
+    return (size_t)SUPER_TILES * (TILE / 2) * (M - 1) * 4 + SUPER_TILES * TILE * 4 +
+           (size_t)TILE * ((M + 3) / 4) * 16;
+}
+
 template <int M>
 __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ rec,
                                                      const uint32_t *__restrict__ qpk,
@@ -490,9 +513,10 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
     constexpr int NV = (M + 3) / 4;
     constexpr int FD = M - 1;
     static_assert(FD >= 1, "packed K1 needs m >= 2");
-    __shared__ uint4 sJ[TILE * NV];
-    __shared__ __align__(16) uint32_t sQ[TILE / 2 * FD];
-    __shared__ int32_t sCnt[TILE];
+    extern __shared__ __align__(16) uint32_t dsm[];
+    uint32_t *sQ = dsm;                                                  // SUPER_TILES x 128 x FD
+    int32_t *sCnt = reinterpret_cast<int32_t *>(dsm + SUPER_TILES * (TILE / 2) * FD);  // SUPER_TILES x 256
+    uint4 *sJ = reinterpret_cast<uint4 *>(sCnt + SUPER_TILES * TILE);    // TILE x NV (general path)
     __shared__ int64_t s_it, s_T;
     const int tid = threadIdx.x, lane = tid & 31;
     const int64_t K = (nT + SUPER_TILES - 1) / SUPER_TILES;
@@ -536,25 +560,31 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
         for (int k = 0; k < FD; ++k)
             P[k] = count_below(lsorted + (T * FD + k) * SUPER, fld(ri, k)) * 0x10001u;
     }
+    // stage the column-pair words of every tile of the item once; zero the counts
+    const int64_t t0 = jt0 - T * SUPER_TILES, nt = jt1 - jt0;  // tile slots [t0, t0 + nt)
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(qpk + jt0 * (TILE / 2) * FD);
+        uint4 *dst = reinterpret_cast<uint4 *>(sQ + t0 * (TILE / 2) * FD);
+        const int n4 = (int)(nt * (TILE / 2) * FD / 4);
+        for (int w = tid; w < n4; w += TILE) dst[w] = src[w];
+        for (int w = tid; w < SUPER_TILES * TILE; w += TILE) sCnt[w] = 0;
+    }
     const uint32_t last_i_id = fld(&rec[(it * TILE + TILE - 1) * NV], M - 1);
     const Transpose32 transpose(lane);
     const int64_t row_off = L.off[it], row_lo = L.lo_w[it], row_stride = L.stride[it];
+    __syncthreads();
     for (int64_t jt = jt0; jt < jt1; ++jt) {
-        __syncthreads();
-#pragma unroll
-        for (int v = 0; v < NV; ++v) sJ[tid * NV + v] = rec[(jt * TILE + tid) * NV + v];
-        for (int w = tid; w < TILE / 2 * FD; w += TILE) sQ[w] = qpk[jt * (TILE / 2) * FD + w];
-        sCnt[tid] = 0;
-        __syncthreads();
+        const int slot = (int)(jt - T * SUPER_TILES);
         // run ids of the two tiles do not overlap -> no duplicate tuples across them
-        const bool disjoint = last_i_id < fld(&sJ[0], M - 1);
+        const bool disjoint = last_i_id < fld(&rec[(jt * TILE) * NV], M - 1);
         uint32_t w[8];
         if (disjoint) {
+            const uint32_t *qt = sQ + slot * (TILE / 2) * FD;
 #pragma unroll
             for (int jw = 0; jw < 8; ++jw) {
                 uint32_t acc = 0;
                 if constexpr (FD == 2) {
-                    const uint4 *q4 = reinterpret_cast<const uint4 *>(sQ) + jw * 8;
+                    const uint4 *q4 = reinterpret_cast<const uint4 *>(qt) + jw * 8;
 #pragma unroll
                     for (int s2 = 0; s2 < 8; ++s2) {
                         const uint4 v = q4[s2];
@@ -562,7 +592,7 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
                         acc = (acc >> 1) + ((v.z - P[0]) & (v.w - P[FD - 1]) & 0x80008000u);
                     }
                 } else {
-                    const uint32_t *q = sQ + jw * 16 * FD;
+                    const uint32_t *q = qt + jw * 16 * FD;
 #pragma unroll
                     for (int s = 0; s < 16; ++s) {
                         uint32_t g = 0x80008000u;
@@ -573,7 +603,11 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
                 }
                 w[jw] = acc;
             }
-        } else {
+        } else {  // (rare) duplicate tuples may straddle the tiles: per-column test with run ids
+            __syncthreads();
+#pragma unroll
+            for (int v = 0; v < NV; ++v) sJ[tid * NV + v] = rec[(jt * TILE + tid) * NV + v];
+            __syncthreads();
 #pragma unroll
             for (int jw = 0; jw < 8; ++jw) {
                 uint32_t acc = 0;
@@ -596,16 +630,20 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
                 const int64_t base = 32 * jw;
                 if (tail < base + 32) w[jw] &= tail <= base ? 0u : (1u << (tail - base)) - 1u;
             }
-            atomicAdd(&sCnt[jw * 32 + lane], __popc(transpose(w[jw])));
         }
         if (row_ok) {
             uint4 *dst = reinterpret_cast<uint4 *>(bits + row_off + (int64_t)tid * row_stride + (8 * jt - row_lo));
             dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
             dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
         }
-        __syncthreads();
-        const int c = sCnt[tid];
-        if (c) atomicAdd(cnt + (jt - L.jt_lo) * TILE + tid, c);
+        transpose8(transpose, w);
+#pragma unroll
+        for (int jw = 0; jw < 8; ++jw) atomicAdd(&sCnt[slot * TILE + jw * 32 + lane], __popc(w[jw]));
+    }
+    __syncthreads();
+    for (int w = tid; w < nt * TILE; w += TILE) {
+        const int c = sCnt[t0 * TILE + w];
+        if (c) atomicAdd(cnt + (jt0 - L.jt_lo) * TILE + w, c);
     }
 }
 
@@ -925,7 +963,10 @@ static int launch_dom(const RankPlan &p, const BitLayout &L, uint32_t *bits, int
 #define PACK_CASE(MM)                                                                              \
     case MM:                                                                                       \
         k_local_ranks<MM - 1><<<dim3((unsigned)K, MM - 1), 256, 0, st>>>(rec, p.Np, p.lsorted, p.qpk); \
-        k_dom_packed<MM><<<g, TILE, 0, st>>>(rec, p.qpk, p.lsorted, N, nT, L, bits, cnt);           \
+        if (packed_smem(MM) > 48 * 1024)                                                           \
+            TEMO_CUDA(cudaFuncSetAttribute(k_dom_packed<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)packed_smem(MM)));                                   \
+        k_dom_packed<MM><<<g, TILE, packed_smem(MM), st>>>(rec, p.qpk, p.lsorted, N, nT, L, bits, cnt); \
         break;
         switch (m) {
             PACK_CASE(2) PACK_CASE(3) PACK_CASE(4) PACK_CASE(5) PACK_CASE(6) PACK_CASE(7) PACK_CASE(8)
