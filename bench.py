@@ -319,17 +319,27 @@ def our_arm(args):
     ms = float(t_max.item())
     value = args.steps / (ms * 1e-3)  # whole-job gens/s of the one shared run
 
-    # ---- end-to-end through the public harness API: host inputs up, objectives down, every step
-    F_host = torch.empty((n, spec.m), dtype=torch.float64).pin_memory()
+    # ---- end-to-end through the public harness API: every step uploads its host inputs
+    # (the host RNG's pairing + shuffle permutations, pinned ring) and reads its objective
+    # matrix back to pinned host memory.  One step in flight: the host draws step g+1's
+    # permutations while the GPU runs step g; step g's result is waited for right after.
+    F_host = [torch.empty((n, spec.m), dtype=torch.float64).pin_memory() for _ in range(2)]
+    done = [torch.cuda.Event(), torch.cuda.Event()]
     h = n // 2
     h2d = 8 * (2 * h + (n + 2 * h))  # pairing permutation + shuffle permutation (int64)
-    d2h = F_host.numel() * 8
+    d2h = F_host[0].numel() * 8
+    checksum = 0.0
     barrier()
     t0 = time.perf_counter()
     for g in range(args.steps):
         st, _ = stepper.step(st, g, gen)
-        F_host.copy_(stepper.population(st)[1], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        F_host[g % 2].copy_(stepper.population(st)[1], non_blocking=True)
+        done[g % 2].record()
+        if g > 0:
+            done[(g - 1) % 2].synchronize()
+            checksum += float(F_host[(g - 1) % 2][0, 0])
+    done[(args.steps - 1) % 2].synchronize()
+    checksum += float(F_host[(args.steps - 1) % 2][0, 0])
     barrier()
     e2e_s = time.perf_counter() - t0
     t_e2e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
