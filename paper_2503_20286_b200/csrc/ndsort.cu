@@ -465,6 +465,21 @@ __global__ void __launch_bounds__(256) k_local_ranks(const uint4 *__restrict__ r
     }
 }
 
+// acc >> 1 plus g: LEA.HI on the ALU pipe, or mad.hi (hi32(acc * 2^31) + g) on the FMA pipe;
+// alternating the two balances the ALU and FMA pipes of the packed K1 inner loop
+#ifndef K1_ACC_MODE
+#define K1_ACC_MODE 1
+#endif
+template <bool FMA>
+__device__ __forceinline__ uint32_t acc_step(uint32_t acc, uint32_t g) {
+    if (FMA) {
+        uint32_t d;
+        asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(acc), "r"(0x80000000u), "r"(g));
+        return d;
+    }
+    return (acc >> 1) + g;
+}
+
 // lower bound count of v in a sorted SUPER-long array
 __device__ __forceinline__ uint32_t count_below(const uint32_t *__restrict__ srt, uint32_t v) {
     int lo = 0;
@@ -588,8 +603,8 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
 #pragma unroll
                     for (int s2 = 0; s2 < 8; ++s2) {
                         const uint4 v = q4[s2];
-                        acc = (acc >> 1) + ((v.x - P[0]) & (v.y - P[FD - 1]) & 0x80008000u);
-                        acc = (acc >> 1) + ((v.z - P[0]) & (v.w - P[FD - 1]) & 0x80008000u);
+                        acc = acc_step<K1_ACC_MODE != 0>(acc, (v.x - P[0]) & (v.y - P[FD - 1]) & 0x80008000u);
+                        acc = acc_step<K1_ACC_MODE == 2>(acc, (v.z - P[0]) & (v.w - P[FD - 1]) & 0x80008000u);
                     }
                 } else {
                     const uint32_t *q = qt + jw * 16 * FD;
@@ -644,6 +659,250 @@ __global__ void __launch_bounds__(TILE) k_dom_packed(const uint4 *__restrict__ r
     for (int w = tid; w < nt * TILE; w += TILE) {
         const int c = sCnt[t0 * TILE + w];
         if (c) atomicAdd(cnt + (jt0 - L.jt_lo) * TILE + w, c);
+    }
+}
+
+// ------------------------------------------------- K1 (packed, 8 rows/lane)
+// k_dom_rows8: same packed test as k_dom_packed, but a warp owns a whole row
+// tile (lane l holds rows 32 r + l, r = 0..7) and a CTA owns 4 row tiles of
+// one column super-tile.  Every broadcast LDS.128 of column-pair words now
+// feeds 8 rows (1 LDS per 32x32 word instead of 8), the super-tile's sorted
+// rank fields are staged once per CTA for the rows' local-rank searches, and
+// the column counts of the 8 row words are first summed bit-sliced per lane
+// (carry-save adders -> 4 slice words) so only 4 warp transposes are needed
+// per 8 row words (instead of 8).
+constexpr int K1W = 4;   // warps = row tiles per CTA
+#ifndef K1_JW_UNROLL
+#define K1_JW_UNROLL 2
+#endif
+constexpr int K1_JWU = K1_JW_UNROLL;
+
+constexpr int RPL = 8;   // rows per lane (TILE / 32)
+
+// sQ | sCnt | union{ sS (sorted fields, only while the rows' local ranks are searched),
+//                     sW (per warp 256 rows x 9 words: row words staged for 32-byte stores) }
+__host__ __device__ constexpr size_t rows8_union(int M) {
+    return (size_t)(M - 1) * SUPER * 4 > (size_t)K1W * TILE * 9 * 4 ? (size_t)(M - 1) * SUPER * 4
+                                                                    : (size_t)K1W * TILE * 9 * 4;
+}
+__host__ __device__ constexpr size_t rows8_smem(int M) {
+    return (size_t)SUPER_TILES * (TILE / 2) * (M - 1) * 4 + (size_t)SUPER_TILES * TILE * 4 + rows8_union(M);
+}
+
+__device__ __forceinline__ uint32_t count_below_s(const uint32_t *srt, uint32_t v) {
+    int lo = 0;
+#pragma unroll
+    for (int step = SUPER / 2; step; step >>= 1)
+        if (srt[lo + step - 1] < v) lo += step;
+    if (srt[lo] < v) ++lo;
+    return (uint32_t)lo;
+}
+
+// bit-sliced sum of 8 words: bit j of out[b] = bit b of (number of inputs with bit j set)
+__device__ __forceinline__ void csa8(const uint32_t x[8], uint32_t out[4]) {
+    auto fa = [](uint32_t a, uint32_t b, uint32_t c, uint32_t &sum, uint32_t &car) {
+        sum = a ^ b ^ c;
+        car = (a & b) | (c & (a ^ b));
+    };
+    uint32_t s1, c1, s2, c2, s3, c3, s5, c5;
+    fa(x[0], x[1], x[2], s1, c1);
+    fa(x[3], x[4], x[5], s2, c2);
+    fa(s1, s2, x[6], s3, c3);
+    out[0] = s3 ^ x[7];
+    const uint32_t c4 = s3 & x[7];
+    fa(c1, c2, c3, s5, c5);
+    out[1] = s5 ^ c4;
+    const uint32_t c6 = s5 & c4;
+    out[2] = c5 ^ c6;
+    out[3] = c5 & c6;
+}
+
+__device__ __forceinline__ void transpose4(const Transpose32 &t, uint32_t x[4]) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        uint32_t y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) y[k] = __shfl_xor_sync(~0u, x[k], 16 >> q);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t r = __funnelshift_l(y[k], y[k], t.rot[q]);
+            uint32_t o;
+            asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(o) : "r"(x[k]), "r"(r), "r"(t.keep[q]));
+            x[k] = o;
+        }
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(K1W * 32, 3) k_dom_rows8(const uint4 *__restrict__ rec,
+                                                           const uint32_t *__restrict__ qpk,
+                                                           const uint32_t *__restrict__ lsorted,
+                                                           int64_t N, int64_t nT, BitLayout L,
+                                                           uint32_t *__restrict__ bits,
+                                                           int32_t *__restrict__ cnt) {
+    constexpr int NV = (M + 3) / 4;
+    constexpr int FD = M - 1;
+    static_assert(FD >= 1, "packed K1 needs m >= 2");
+    extern __shared__ __align__(16) uint32_t dsm[];
+    uint32_t *sQ = dsm;                                                         // SUPER_TILES x 128 x FD
+    int32_t *sCnt = reinterpret_cast<int32_t *>(sQ + SUPER_TILES * (TILE / 2) * FD);  // SUPER_TILES x TILE
+    uint32_t *sS = reinterpret_cast<uint32_t *>(sCnt + SUPER_TILES * TILE);    // FD x SUPER (phase 1)
+    uint32_t *sW = sS;                                                          // K1W x TILE x 9 (phase 2)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int64_t T, g;
+    if (!L.grid2d) {
+        // super-tile T has 2T + 2 items (row-tile groups) -> items before T = T (T + 1)
+        const int64_t item = blockIdx.x;
+        int64_t t = (int64_t)((sqrt(4.0 * (double)item + 1.0) - 1.0) * 0.5);
+        while (t * (t + 1) > item) --t;
+        while ((t + 1) * (t + 2) <= item) ++t;
+        T = t;
+        g = item - t * (t + 1);
+    } else {
+        T = L.jt_lo / SUPER_TILES + blockIdx.x;
+        g = blockIdx.y;
+    }
+    const int64_t ct0 = max(T * SUPER_TILES, L.jt_lo);                // column tiles of the CTA
+    const int64_t ct1 = min(min((T + 1) * SUPER_TILES, L.jt_hi), nT);
+    const int64_t it0 = g * K1W;
+    if (ct0 >= ct1 || it0 >= ct1) return;
+    {
+        const int64_t s0 = ct0 - T * SUPER_TILES;
+        const uint4 *src = reinterpret_cast<const uint4 *>(qpk + ct0 * (TILE / 2) * FD);
+        uint4 *dst = reinterpret_cast<uint4 *>(sQ + s0 * (TILE / 2) * FD);
+        const int n4 = (int)((ct1 - ct0) * (TILE / 2) * FD / 4);
+        for (int w = tid; w < n4; w += K1W * 32) dst[w] = src[w];
+        const uint4 *ss = reinterpret_cast<const uint4 *>(lsorted + T * FD * SUPER);
+        uint4 *sd = reinterpret_cast<uint4 *>(sS);
+        for (int w = tid; w < FD * SUPER / 4; w += K1W * 32) sd[w] = ss[w];
+        for (int w = tid; w < SUPER_TILES * TILE; w += K1W * 32) sCnt[w] = 0;
+    }
+    __syncthreads();
+    const int64_t it = it0 + warp;
+    const int64_t jt0 = max(ct0, it), jt1 = ct1;
+    const bool active = it < nT && jt0 < jt1;
+    // this lane's rows it*256 + 32 r + lane: local ranks (both halves) and validity
+    uint32_t P[RPL][FD];
+    uint32_t row_ok = 0;
+    if (active) {
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+            const int64_t i = it * TILE + 32 * r + lane;
+            row_ok |= (uint32_t)(i < N) << r;
+            uint4 ri[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) ri[v] = rec[i * NV + v];
+#pragma unroll
+            for (int k = 0; k < FD; ++k) P[r][k] = count_below_s(sS + k * SUPER, fld(ri, k)) * 0x10001u;
+        }
+    }
+    __syncthreads();  // sS is dead from here on; its space becomes sW
+    if (active) {
+        const uint32_t last_i_id = fld(&rec[(it * TILE + TILE - 1) * NV], M - 1);
+        const Transpose32 transpose(lane);
+        const int64_t row_off = L.off[it], row_lo = L.lo_w[it], row_stride = L.stride[it];
+        for (int64_t jt = jt0; jt < jt1; ++jt) {
+            const int slot = (int)(jt - T * SUPER_TILES);
+            const bool disjoint = last_i_id < fld(&rec[(jt * TILE) * NV], M - 1);
+            const int64_t tail = N - jt * TILE;  // columns past N are masked
+            const uint32_t *qt = sQ + slot * (TILE / 2) * FD;
+            const uint4 *sj = rec + jt * TILE * NV;  // (rare path) column records straight from L1/L2
+            uint32_t *sw = sW + warp * TILE * 9 + lane * 9;  // row 32 r + lane at sw + 32 * 9 r
+#pragma unroll K1_JWU
+            for (int jw = 0; jw < 8; ++jw) {
+                uint32_t acc[RPL];
+#pragma unroll
+                for (int r = 0; r < RPL; ++r) acc[r] = 0;
+                if (disjoint) {
+                    if constexpr (FD == 2) {
+                        const uint4 *q4 = reinterpret_cast<const uint4 *>(qt) + jw * 8;
+#pragma unroll
+                        for (int s2 = 0; s2 < 8; ++s2) {
+                            const uint4 v = q4[s2];
+#pragma unroll
+                            for (int r = 0; r < RPL; ++r) {
+                                acc[r] = acc_step<false>(acc[r], (v.x - P[r][0]) & (v.y - P[r][FD - 1]) & 0x80008000u);
+                                acc[r] = acc_step<false>(acc[r], (v.z - P[r][0]) & (v.w - P[r][FD - 1]) & 0x80008000u);
+                            }
+                        }
+                    } else {
+                        const uint32_t *q = qt + jw * 16 * FD;
+#pragma unroll
+                        for (int st = 0; st < 16; ++st) {
+                            uint32_t qv[FD];
+#pragma unroll
+                            for (int k = 0; k < FD; ++k) qv[k] = q[st * FD + k];
+#pragma unroll
+                            for (int r = 0; r < RPL; ++r) {
+                                uint32_t gg = 0x80008000u;
+#pragma unroll
+                                for (int k = 0; k < FD; ++k) gg &= qv[k] - P[r][k];
+                                acc[r] = acc_step<false>(acc[r], gg);
+                            }
+                        }
+                    }
+                } else {
+#pragma unroll 1
+                    for (int r = 0; r < RPL; ++r) {
+                        const int64_t i = it * TILE + 32 * r + lane;
+                        uint32_t nf[4 * NV];
+                        uint4 ri[NV];
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) ri[v] = rec[i * NV + v];
+#pragma unroll
+                        for (int k = 0; k < 4 * NV; ++k) nf[k] = 0u - fld(ri, k);
+                        nf[M - 1] -= 1u;
+                        uint32_t a = 0;
+#pragma unroll 4
+                        for (int b = 0; b < 32; ++b) {
+                            const uint4 *v = &sj[(jw * 32 + b) * NV];
+                            uint32_t x = fld(v, M - 1) + nf[M - 1];
+#pragma unroll
+                            for (int k = 0; k < M - 1; ++k) x |= fld(v, k) + nf[k];
+                            a = __funnelshift_l(x, a, 1);
+                        }
+#pragma unroll
+                        for (int r2 = 0; r2 < RPL; ++r2)
+                            if (r2 == r) acc[r2] = __brev(~a);
+                    }
+                }
+                // masks: rows past N, columns past N
+                uint32_t cm = ~0u;
+                if (tail < TILE) {
+                    const int64_t base = 32 * jw;
+                    if (tail < base + 32) cm = tail <= base ? 0u : (1u << (tail - base)) - 1u;
+                }
+#pragma unroll
+                for (int r = 0; r < RPL; ++r) acc[r] &= ((row_ok >> r) & 1) ? cm : 0u;
+#pragma unroll
+                for (int r = 0; r < RPL; ++r) sw[32 * 9 * r + jw] = acc[r];
+                // column counts over the warp's 256 rows: bit-sliced sum of 8 rows, 4 transposes
+                uint32_t sl[4];
+                csa8(acc, sl);
+                transpose4(transpose, sl);
+                const int c = __popc(sl[0]) + 2 * __popc(sl[1]) + 4 * __popc(sl[2]) + 8 * __popc(sl[3]);
+                atomicAdd(&sCnt[slot * TILE + jw * 32 + lane], c);
+            }
+            __syncwarp();
+            // each lane writes its 8 rows' 8 words for this tile as two 16-byte stores per row
+            uint32_t *rowp = bits + row_off + (int64_t)lane * row_stride + (8 * jt - row_lo);
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) {
+                const uint32_t *x = sw + 32 * 9 * r;
+                if ((row_ok >> r) & 1) {
+                    uint4 *dst = reinterpret_cast<uint4 *>(rowp + (int64_t)(32 * r) * row_stride);
+                    dst[0] = make_uint4(x[0], x[1], x[2], x[3]);
+                    dst[1] = make_uint4(x[4], x[5], x[6], x[7]);
+                }
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    const int64_t s0 = ct0 - T * SUPER_TILES;
+    for (int w = tid; w < (ct1 - ct0) * TILE; w += K1W * 32) {
+        const int c = sCnt[s0 * TILE + w];
+        if (c) atomicAdd(cnt + (ct0 - L.jt_lo) * TILE + w, c);
     }
 }
 
@@ -899,6 +1158,16 @@ static bool packed_disabled() {
     return v == 1;
 }
 
+// TEMO_K1_ROWS8=0 selects the 1-row-per-lane packed kernel (A/B comparisons)
+static bool rows8_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_K1_ROWS8");
+        v = (e && e[0] == '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 static inline dim3 grid1(int64_t n, int t = 256) { return dim3((unsigned)((n + t - 1) / t)); }
 
 // K0: column ranks, lex order (p.vals_a), run ids and records (p.rec)
@@ -963,6 +1232,20 @@ static int launch_dom(const RankPlan &p, const BitLayout &L, uint32_t *bits, int
 #define PACK_CASE(MM)                                                                              \
     case MM:                                                                                       \
         k_local_ranks<MM - 1><<<dim3((unsigned)K, MM - 1), 256, 0, st>>>(rec, p.Np, p.lsorted, p.qpk); \
+        if (MM <= 5 && !rows8_disabled()) {                                                        \
+            dim3 g8;                                                                               \
+            if (L.grid2d) {                                                                        \
+                const int64_t T0 = L.jt_lo / SUPER_TILES, T1 = (L.jt_hi + SUPER_TILES - 1) / SUPER_TILES; \
+                g8 = dim3((unsigned)(T1 - T0), (unsigned)((L.jt_hi + K1W - 1) / K1W));              \
+            } else {                                                                               \
+                g8 = dim3((unsigned)(K * (K + 1)));                                                \
+            }                                                                                      \
+            if (rows8_smem(MM) > 48 * 1024)                                                        \
+                TEMO_CUDA(cudaFuncSetAttribute(k_dom_rows8<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                               (int)rows8_smem(MM)));                              \
+            k_dom_rows8<MM><<<g8, K1W * 32, rows8_smem(MM), st>>>(rec, p.qpk, p.lsorted, N, nT, L, bits, cnt); \
+            break;                                                                                 \
+        }                                                                                          \
         if (packed_smem(MM) > 48 * 1024)                                                           \
             TEMO_CUDA(cudaFuncSetAttribute(k_dom_packed<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                            (int)packed_smem(MM)));                                   \
