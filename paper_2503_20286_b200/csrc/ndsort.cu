@@ -676,6 +676,12 @@ constexpr int K1W = 4;   // warps = row tiles per CTA
 #define K1_JW_UNROLL 2
 #endif
 constexpr int K1_JWU = K1_JW_UNROLL;
+#ifndef K1_R8_MINB
+#define K1_R8_MINB 4
+#endif
+#ifndef K1_R8_FMA
+#define K1_R8_FMA 0
+#endif
 
 constexpr int RPL = 8;   // rows per lane (TILE / 32)
 
@@ -734,7 +740,7 @@ __device__ __forceinline__ void transpose4(const Transpose32 &t, uint32_t x[4]) 
 }
 
 template <int M>
-__global__ void __launch_bounds__(K1W * 32, 3) k_dom_rows8(const uint4 *__restrict__ rec,
+__global__ void __launch_bounds__(K1W * 32, K1_R8_MINB) k_dom_rows8(const uint4 *__restrict__ rec,
                                                            const uint32_t *__restrict__ qpk,
                                                            const uint32_t *__restrict__ lsorted,
                                                            int64_t N, int64_t nT, BitLayout L,
@@ -821,8 +827,8 @@ __global__ void __launch_bounds__(K1W * 32, 3) k_dom_rows8(const uint4 *__restri
                             const uint4 v = q4[s2];
 #pragma unroll
                             for (int r = 0; r < RPL; ++r) {
-                                acc[r] = acc_step<false>(acc[r], (v.x - P[r][0]) & (v.y - P[r][FD - 1]) & 0x80008000u);
-                                acc[r] = acc_step<false>(acc[r], (v.z - P[r][0]) & (v.w - P[r][FD - 1]) & 0x80008000u);
+                                acc[r] = acc_step<K1_R8_FMA >= 2>(acc[r], (v.x - P[r][0]) & (v.y - P[r][FD - 1]) & 0x80008000u);
+                                acc[r] = acc_step<K1_R8_FMA >= 1>(acc[r], (v.z - P[r][0]) & (v.w - P[r][FD - 1]) & 0x80008000u);
                             }
                         }
                     } else {

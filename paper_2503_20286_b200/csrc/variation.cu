@@ -688,11 +688,20 @@ __global__ void __launch_bounds__(OW * 32, OFF_MINB) k_offspring_w(temo_problem 
 //   - SBX pows compacted across the warp: only crossed genes (about half)
 //     are queued in shared memory and every lane takes queue slots, so a
 //     warp round issues ceil(#crossed/32) pows instead of 4.
+#ifndef OFF_S_MINB
+#define OFF_S_MINB 2
+#endif
 constexpr int SW = 8;            // warps per CTA
+
+// SBX spread factor of one crossed gene (variation.py:77-78); out of line so pow's
+// internal registers do not inflate the register budget of the offspring kernel
+__device__ __noinline__ double sbx_beta(double mu, double e) {
+    return pow((0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu), e);
+}
 constexpr int SMAX_D = 3000;     // genes staged in shared memory (else k_offspring_w)
 
 template <int M, bool SWAP>
-__global__ void __launch_bounds__(SW * 32, 2) k_offspring_s(temo_problem P, VarArgs V,
+__global__ void __launch_bounds__(SW * 32, OFF_S_MINB) k_offspring_s(temo_problem P, VarArgs V,
                                                             const double *__restrict__ X,
                                                             const int64_t *__restrict__ i1,
                                                             const int64_t *__restrict__ i2, int64_t h,
@@ -729,6 +738,10 @@ __global__ void __launch_bounds__(SW * 32, 2) k_offspring_s(temo_problem P, VarA
     const double e = 1.0 / (V.eta_c + 1.0);
     const double eta = V.eta_m + 1.0;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    // U = k 2^-53 <= p_m  <=>  k <= floor(p_m 2^53)  (p_m - U >= 0 is exact for doubles)
+    int64_t pm_thr = -1;
+    if (V.p_m >= 1.0) pm_thr = INT64_MAX;
+    else if (V.p_m >= 0.0) pm_thr = (int64_t)floor(V.p_m * 9007199254740992.0);
     for (int64_t q = (int64_t)blockIdx.x * SW + (threadIdx.x >> 5); q < h; q += (int64_t)gridDim.x * SW) {
         const double *x1 = X + i1[q] * d;
         const double *x2 = X + i2[q] * d;
@@ -742,41 +755,24 @@ __global__ void __launch_bounds__(SW * 32, 2) k_offspring_s(temo_problem P, VarA
         for (int64_t base = -sh; base < d; base += 128) {
             const int64_t gs = base + 4 * lane;
             const int64_t es = q * d + gs;
-            constexpr int NS = SWAP ? 5 : 3;
-            constexpr int NA = NS - 2;
-            uint64_t R[NS][4];
-            {
-                int64_t E[NA];
-                if (SWAP) {
-                    E[0] = o_cross + es;
-                    E[1] = o_swap + es;
-                }
-                E[NA - 1] = o_mu + es;
-                raw_quads<NA>(ph, E, avail, R);
-                const int64_t EH[2] = {o_hit + es, o_hit + hd + es};  // (second unused in single mode)
-                raw_quads<2>(ph, EH, avail, R + NA);
-            }
-            double a[4], b[4], c1[4], c2[4];
+            // randomness first, in phases that keep few raw words live:
+            //   cross/swap (top bits) -> mu of crossed genes into the warp's pow queue -> hit bits
             bool ok[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int64_t g = gs + k;
-                ok[k] = g >= 0 && g < d;
-                a[k] = ok[k] ? __ldg(x1 + g) : 0.0;
-                b[k] = ok[k] ? __ldg(x2 + g) : 0.0;
-            }
-            // --- SBX (variation.py:72-91): crossed / swap are top-bit tests of the raw words
+            for (int k = 0; k < 4; ++k) ok[k] = gs + k >= 0 && gs + k < d;
             uint32_t crossed = 0xF, negate = 0;
             if (SWAP) {
+                uint64_t R[2][4];
+                const int64_t E[2] = {o_cross + es, o_swap + es};
+                raw_quads<2>(ph, E, avail, R);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    crossed &= ~((uint32_t)(R[0][k] >> 63) << k);
+                    crossed &= ~((uint32_t)(R[0][k] >> 63) << k);  // U < 0.5 <=> top bit 0
                     negate |= (uint32_t)(1u - (uint32_t)(R[1][k] >> 63)) << k;
                 }
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) crossed &= (uint32_t)ok[k] << k | ~(1u << k);
-            // queue the crossed genes' mu, pow them warp-wide, read the betas back
             const int nq = __popc(crossed);
             int incl = nq;
 #pragma unroll
@@ -786,15 +782,34 @@ __global__ void __launch_bounds__(SW * 32, 2) k_offspring_s(temo_problem P, VarA
             }
             const int total = __shfl_sync(~0u, incl, 31);
             int slot = incl - nq;
+            {
+                uint64_t R[1][4];
+                const int64_t E[1] = {o_mu + es};
+                raw_quads<1>(ph, E, avail, R);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if ((crossed >> k) & 1) s_q[slot++] = u01(R[NA - 1][k]);
-            __syncwarp();
-            for (int t = lane; t < total; t += 32) {
-                const double mu = s_q[t];
-                s_q[t] = pow((0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu), e);
+                for (int k = 0; k < 4; ++k)
+                    if ((crossed >> k) & 1) s_q[slot++] = u01(R[0][k]);
+            }
+            uint32_t hit = 0;  // PM hit (p_m - U >= 0) as an integer test on the raw word
+            {
+                uint64_t R[2][4];
+                const int64_t E[2] = {o_hit + es, o_hit + hd + es};  // (second unused in single mode)
+                raw_quads<2>(ph, E, avail, R);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    hit |= (uint32_t)(ok[k] && (int64_t)(R[0][k] >> 11) <= pm_thr) << k;
+                    if (!single) hit |= (uint32_t)(ok[k] && (int64_t)(R[1][k] >> 11) <= pm_thr) << (4 + k);
+                }
             }
             __syncwarp();
+            for (int t = lane; t < total; t += 32) s_q[t] = sbx_beta(s_q[t], e);
+            __syncwarp();
+            double a[4], b[4], c1[4], c2[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                a[k] = ok[k] ? __ldg(x1 + gs + k) : 0.0;
+                b[k] = ok[k] ? __ldg(x2 + gs + k) : 0.0;
+            }
             slot = incl - nq;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -818,12 +833,6 @@ __global__ void __launch_bounds__(SW * 32, 2) k_offspring_s(temo_problem P, VarA
             __syncwarp();  // s_q reused next round
             (void)lt_mask;
             // --- polynomial mutation (variation.py:104-120), only where hit
-            uint32_t hit = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                hit |= (uint32_t)(ok[k] && V.p_m - u01(R[NS - 2][k]) >= 0.0) << k;
-                if (!single) hit |= (uint32_t)(ok[k] && V.p_m - u01(R[NS - 1][k]) >= 0.0) << (4 + k);
-            }
             if (hit) {
                 uint64_t m1[4], m2[4];
                 if (hit & 0xF) raw_quad(ph, o_pmu + es, avail, m1);
