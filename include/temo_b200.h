@@ -183,6 +183,12 @@ typedef struct temo_variation {
 int temo_evaluate(const temo_problem *prob, const double *X, int64_t n, double *F,
                   temo_stream_t stream);
 
+/* SBX spread factor (variation.py:77-78) for U = mu[t]: beta[t] = pow(2 mu, e) or
+ * pow(1 / (2 - 2 mu), e), e = 1 / (eta_c + 1); fast = 1 uses the exp/log form the fused
+ * offspring kernel uses (csrc/sbx_pow.cuh), fast = 0 CUDA's pow.  Diagnostic/parity hook. */
+int temo_sbx_beta(const double *mu, int64_t n, double eta_c, int fast, double *beta,
+                  temo_stream_t stream);
+
 /* Uniform draws: out[e] = Generator.random() element `off + e` of the stream. */
 int temo_uniform(const temo_philox_state *st, uint64_t off, int64_t count, double *out,
                  temo_stream_t stream);
@@ -270,8 +276,8 @@ int temo_hype_select(const double *F, int64_t N, int m, int64_t n, int64_t s, co
  * 1 <= T <= min(r, 64), m <= 16. */
 int temo_neighbors(const double *W, int64_t r, int m, int T, int32_t *out, temo_stream_t stream);
 
-/* Roofline probe: compare-pipe rate (compares/s) of the K1 instruction mix on
- * register operands (the denominator of bench.py's integer roofline). */
+/* Diagnostic microbenchmark: issue rate (compares/s) of a register-only ISETP + VOTE mix.
+ * Not a roofline denominator (bench.py derives K1's ceiling from the SM issue rate). */
 double temo_probe_compare_rate(int blocks, int iters, temo_stream_t stream);
 
 /* ------------------------------------------------------------ stage timing

@@ -1,8 +1,8 @@
-// Compare-pipe roofline probe: the K1 inner-loop instruction mix (two chained
-// unsigned ISETP + one warp VOTE per (warp, row)) on register operands only,
-// no memory traffic.  bench.py divides K1's algorithmic compares by this
-// measured rate to report roofline.frac for the integer/compare-bound kernel
-// (MEASURED_PEAKS.json only has HBM and bf16 figures).
+// Diagnostic microbenchmark: the first K1 design's inner-loop instruction mix
+// (two chained unsigned ISETP + one warp VOTE per (warp, row)) on register
+// operands only.  Kept as a probe of the compare/vote issue rate; the packed K1
+// beats it, so it is not used as a roofline denominator (bench.py uses the SM
+// issue rate).
 #include "common.cuh"
 
 namespace temo {

@@ -1,0 +1,84 @@
+// SBX spread factor beta = base^e (variation.py:77-78) without the general pow.
+//
+//   mu <= 0.5 : base = 2 mu           -> beta = exp( e * log(2 mu))
+//   mu >  0.5 : base = 1 / (2 - 2 mu) -> beta = exp(-e * log(2 - 2 mu))
+//
+// 2 mu and 2 - 2 mu = 2 (1 - mu) are exact for mu = k 2^-53 (Sterbenz), so the
+// only roundings are the ones below; the reciprocal of the reference is folded
+// into the sign of the logarithm.  log: frexp reduction to m in [sqrt(1/2), sqrt(2)),
+// log m = 2 atanh(s), s = (m-1)/(m+1), |s| <= 0.1716, odd series to s^23
+// (truncation < 2e-18); k ln2 split hi/lo.  exp: n = rint(y log2 e), Cody-Waite
+// r = y - n ln2 (|r| <= 0.35), Taylor to r^13 (< 1e-17), 2^n by exponent add.
+// About 60 instructions instead of ~300 for CUDA's pow; |rel err| of beta is a
+// few ulp (< 1.5e-15 against np.power on 10^6 draws and the edge cases,
+// tests/test_gpu_variation.py::test_sbx_beta_fast_vs_numpy).  Measured on B200
+// it does NOT speed up k_offspring_s (6.0 vs 5.3 ms at pop 200k: the kernel is
+// latency-bound, and the division plus frexp/ldexp lengthen the dependent
+// chain), so the kernel keeps CUDA's pow (OFF_FAST_POW = 0); this form stays as
+// a tested option.
+#pragma once
+
+namespace temo {
+
+__device__ __forceinline__ double log_pos_fast(double x) {  // x > 0, finite, normal
+    const double LN2_HI = 6.93147180369123816490e-01;     // 0x3FE62E42FEE00000
+    const double LN2_LO = 1.90821492927058770002e-10;     // 0x3DEA39EF35793C76
+    int k;
+    double m = frexp(x, &k);  // m in [0.5, 1)
+    if (m < 0.70710678118654752440) {
+        m = m + m;
+        k -= 1;
+    }
+    const double s = (m - 1.0) / (m + 1.0);
+    const double z = s * s;
+    // 2 atanh(s) = 2 s + 2 s^3 (1/3 + z/5 + ... + z^10/23)
+    double p = 1.0 / 23.0;
+    p = fma(p, z, 1.0 / 21.0);
+    p = fma(p, z, 1.0 / 19.0);
+    p = fma(p, z, 1.0 / 17.0);
+    p = fma(p, z, 1.0 / 15.0);
+    p = fma(p, z, 1.0 / 13.0);
+    p = fma(p, z, 1.0 / 11.0);
+    p = fma(p, z, 1.0 / 9.0);
+    p = fma(p, z, 1.0 / 7.0);
+    p = fma(p, z, 1.0 / 5.0);
+    p = fma(p, z, 1.0 / 3.0);
+    const double t = 2.0 * s;
+    const double lm = fma(t * z, p, t);
+    const double kd = (double)k;
+    return fma(kd, LN2_HI, fma(kd, LN2_LO, lm));
+}
+
+__device__ __forceinline__ double exp_fast(double y) {  // |y| < 700
+    const double LOG2E = 1.44269504088896338700e+00;
+    const double LN2_HI = 6.93147180369123816490e-01;
+    const double LN2_LO = 1.90821492927058770002e-10;
+    const double n = rint(y * LOG2E);
+    const double r = fma(-n, LN2_LO, fma(-n, LN2_HI, y));
+    double p = 1.0 / 6227020800.0;  // 1/13!
+    p = fma(p, r, 1.0 / 479001600.0);
+    p = fma(p, r, 1.0 / 39916800.0);
+    p = fma(p, r, 1.0 / 3628800.0);
+    p = fma(p, r, 1.0 / 362880.0);
+    p = fma(p, r, 1.0 / 40320.0);
+    p = fma(p, r, 1.0 / 5040.0);
+    p = fma(p, r, 1.0 / 720.0);
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    return ldexp(p, (int)n);
+}
+
+// beta of one crossed gene (mu = U in [0, 1), e = 1 / (eta_c + 1) > 0)
+__device__ __forceinline__ double sbx_beta_fast(double mu, double e) {
+    if (0.5 - mu >= 0.0) {
+        if (mu == 0.0) return 0.0;  // pow(0, e) = 0
+        return exp_fast(e * log_pos_fast(2.0 * mu));
+    }
+    return exp_fast(-e * log_pos_fast(2.0 - 2.0 * mu));
+}
+
+}  // namespace temo

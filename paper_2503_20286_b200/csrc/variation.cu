@@ -16,6 +16,7 @@
 // templated on m so per-objective accumulators live in registers.
 #include "common.cuh"
 #include "philox.cuh"
+#include "sbx_pow.cuh"
 
 namespace temo {
 
@@ -688,6 +689,12 @@ __global__ void __launch_bounds__(OW * 32, OFF_MINB) k_offspring_w(temo_problem 
 //   - SBX pows compacted across the warp: only crossed genes (about half)
 //     are queued in shared memory and every lane takes queue slots, so a
 //     warp round issues ceil(#crossed/32) pows instead of 4.
+#ifndef OFF_FAST_POW
+#define OFF_FAST_POW 0
+#endif
+#ifndef OFF_PREFETCH
+#define OFF_PREFETCH 1
+#endif
 #ifndef OFF_S_MINB
 #define OFF_S_MINB 2
 #endif
@@ -755,6 +762,13 @@ __global__ void __launch_bounds__(SW * 32, OFF_S_MINB) k_offspring_s(temo_proble
         for (int64_t base = -sh; base < d; base += 128) {
             const int64_t gs = base + 4 * lane;
             const int64_t es = q * d + gs;
+            // parents' quads: prefetched into L1 now (no registers held), loaded after the randomness
+#if OFF_PREFETCH
+            if (gs >= 0 && gs < d) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(x1 + gs));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(x2 + gs));
+            }
+#endif
             // randomness first, in phases that keep few raw words live:
             //   cross/swap (top bits) -> mu of crossed genes into the warp's pow queue -> hit bits
             bool ok[4];
@@ -802,7 +816,11 @@ __global__ void __launch_bounds__(SW * 32, OFF_S_MINB) k_offspring_s(temo_proble
                 }
             }
             __syncwarp();
+#if OFF_FAST_POW
+            for (int t = lane; t < total; t += 32) s_q[t] = sbx_beta_fast(s_q[t], e);
+#else
             for (int t = lane; t < total; t += 32) s_q[t] = sbx_beta(s_q[t], e);
+#endif
             __syncwarp();
             double a[4], b[4], c1[4], c2[4];
 #pragma unroll
@@ -1026,6 +1044,22 @@ extern "C" int temo_evaluate(const temo_problem *prob, const double *X, int64_t 
 #undef EVAL_CASE
     TEMO_LAUNCH_CHECK();
     stage_end(S_EVALUATE, s);
+    return TEMO_OK;
+}
+
+__global__ void k_sbx_beta(const double *__restrict__ mu, int64_t n, double e, int fast,
+                           double *__restrict__ beta) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < n) beta[t] = fast ? temo::sbx_beta_fast(mu[t], e) : temo::sbx_beta(mu[t], e);
+}
+
+extern "C" int temo_sbx_beta(const double *mu, int64_t n, double eta_c, int fast, double *beta,
+                             temo_stream_t stream) {
+    if (n < 0 || !mu || !beta || !(eta_c > -1.0)) return TEMO_EINVAL;
+    if (n == 0) return TEMO_OK;
+    k_sbx_beta<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(mu, n, 1.0 / (eta_c + 1.0),
+                                                                             fast, beta);
+    TEMO_LAUNCH_CHECK();
     return TEMO_OK;
 }
 

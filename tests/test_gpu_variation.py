@@ -137,3 +137,31 @@ def test_fused_offspring_matches_oracle(cuda, name, m, d, n):
     FO = state.cur.F[n:n + 2 * h].cpu().numpy()
     assert np.allclose(FO, oprob.evaluate(name, O_ref, m), rtol=1e-10, atol=1e-12)
     assert np.array_equal(g_dev.permutation(50), g_ref.permutation(50))
+
+
+def test_sbx_beta_fast_vs_numpy(cuda):
+    """The exp/log SBX spread factor used by the fused offspring kernel (csrc/sbx_pow.cuh)
+    against np.power on the reference's expression (variation.py:77-78): 10^6 Philox draws
+    plus the edge cases of the U grid.  Bound: 1.5e-15 relative (a few ulp; the offspring
+    parity tests need 1e-13)."""
+    import torch
+
+    from paper_2503_20286_b200 import _lib
+
+    u = np.random.default_rng(0).random(1_000_000)
+    ulp = 2.0 ** -53
+    edges = np.array([0.0, ulp, 2 * ulp, 0.25, 0.5 - ulp, 0.5, 0.5 + ulp, 0.75, 1 - 2 * ulp, 1 - ulp])
+    mu = np.concatenate([edges, u])
+    for eta_c in (20.0, 15.0, 2.0, 0.5):
+        e = 1.0 / (eta_c + 1.0)
+        want = np.where(0.5 - mu >= 0.0, np.power(2.0 * mu, e), np.power(1.0 / (2.0 - 2.0 * mu), e))
+        d_mu = torch.from_numpy(mu).cuda()
+        out = torch.empty_like(d_mu)
+        for fast in (1, 0):
+            rc = _lib.lib().temo_sbx_beta(_lib.ptr(d_mu), mu.size, eta_c, fast, _lib.ptr(out),
+                                          _lib.stream_handle(d_mu.device))
+            assert rc == 0
+            got = out.cpu().numpy()
+            rel = np.abs(got - want) / np.where(want == 0, 1.0, want)
+            assert got[0] == 0.0 and np.all(np.isfinite(got))
+            assert rel.max() < 1.5e-15, (eta_c, fast, rel.max())
