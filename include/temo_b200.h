@@ -215,6 +215,17 @@ int temo_offspring(const temo_problem *prob, const temo_variation *var, const do
                    const int64_t *i1, const int64_t *i2, int64_t h, const temo_philox_state *st,
                    uint64_t off, double *O, double *FO, temo_stream_t stream);
 
+/* Same result as temo_offspring, computed in two phases through caller workspace
+ * (temo_offspring_ws_bytes(h, d) bytes: h*d betas + per-quad flags): a pure-randomness
+ * kernel (Philox draws, SBX betas of crossed genes, PM hit bits) and a streaming apply
+ * kernel (parents -> children -> objectives).  Falls back to the fused kernel when the
+ * streams are not congruent mod 4 or d is above the staged-constant limit. */
+size_t temo_offspring_ws_bytes(int64_t h, int64_t d);
+int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const double *X,
+                      const int64_t *i1, const int64_t *i2, int64_t h, const temo_philox_state *st,
+                      uint64_t off, double *O, double *FO, void *ws, size_t ws_bytes,
+                      temo_stream_t stream);
+
 /* ------------------------------------------------------------------ MOEA/D
  * temo_moead_offspring: moead.moead_offspring (moead.py:127-145) for parents
  *   p1[i], p2[i] (rows of X): SBX child c1 only, PM, evaluate -> O, FO (n rows);

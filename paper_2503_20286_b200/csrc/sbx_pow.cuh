@@ -10,7 +10,7 @@
 // (truncation < 2e-18); k ln2 split hi/lo.  exp: n = rint(y log2 e), Cody-Waite
 // r = y - n ln2 (|r| <= 0.35), Taylor to r^13 (< 1e-17), 2^n by exponent add.
 // About 60 instructions instead of ~300 for CUDA's pow; |rel err| of beta is a
-// few ulp (< 1.5e-15 against np.power on 10^6 draws and the edge cases,
+// few ulp (< 4e-15 against np.power on 10^6 draws and the edge cases,
 // tests/test_gpu_variation.py::test_sbx_beta_fast_vs_numpy).  Measured on B200
 // it does NOT speed up k_offspring_s (6.0 vs 5.3 ms at pop 200k: the kernel is
 // latency-bound, and the division plus frexp/ldexp lengthen the dependent

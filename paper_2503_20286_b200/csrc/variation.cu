@@ -925,6 +925,252 @@ __global__ void __launch_bounds__(SW * 32, OFF_S_MINB) k_offspring_s(temo_proble
     }
 }
 
+// ---------------------------------------------- two-phase offspring (ws)
+// Phase 1 `k_offspring_rand`: pure randomness, no population traffic.  Warp per
+// pair, lane per Philox-aligned quad as above; per quad it emits one flag word
+// (crossed | hit c1 << 4 | hit c2 << 8) and, for crossed genes, beta (sign of
+// the swap folded in) into a pair-major array.  The SBX pows of a warp round
+// are queued (gene, mu) in shared memory and spread over all lanes, each lane
+// writing its results straight to global memory.  Small register footprint ->
+// high occupancy for the serial Philox and pow chains.
+// Phase 2 `k_offspring_apply`: parents, flags and betas in, children and
+// objectives out (PM's rare mu draws on the spot) -- a streaming kernel.
+#ifndef OFF_APPLY_MINB
+#define OFF_APPLY_MINB 2
+#endif
+constexpr int RW = 8;  // warps per CTA of both phases
+
+__host__ __device__ inline int64_t quads_per_pair(int64_t d) { return (d + 3) / 4 + 1; }
+
+template <bool SWAP>
+__global__ void __launch_bounds__(RW * 32, 4) k_offspring_rand(int64_t d, VarArgs V, int64_t h, Philox ph,
+                                                               uint64_t off, int single,
+                                                               double *__restrict__ beta,
+                                                               uint16_t *__restrict__ flags) {
+    __shared__ double s_mu[RW][128];
+    __shared__ int32_t s_g[RW][128];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t hd = h * d;
+    const int64_t o_mu = (int64_t)off, o_swap = o_mu + hd, o_cross = o_mu + (SWAP ? 2 * hd : 0);
+    const int64_t o_pmu = o_mu + (SWAP ? 3 * hd : hd);
+    const int64_t o_hit = o_pmu + (single ? hd : 2 * hd);
+    const int64_t avail = 4 - ph.pos;
+    const double e = 1.0 / (V.eta_c + 1.0);
+    int64_t pm_thr = -1;
+    if (V.p_m >= 1.0) pm_thr = INT64_MAX;
+    else if (V.p_m >= 0.0) pm_thr = (int64_t)floor(V.p_m * 9007199254740992.0);
+    const int64_t QP = quads_per_pair(d);
+    for (int64_t q = (int64_t)blockIdx.x * RW + warp; q < h; q += (int64_t)gridDim.x * RW) {
+        const int sh = (int)((o_mu + q * d - avail) & 3);
+        double *bq = beta + q * d;
+        for (int64_t base = -sh, j0 = 0; base < d; base += 128, j0 += 32) {
+            const int64_t gs = base + 4 * lane;
+            const int64_t es = q * d + gs;
+            uint32_t okm = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) okm |= (uint32_t)(gs + k >= 0 && gs + k < d) << k;
+            uint32_t crossed = okm, negate = 0;
+            if (SWAP) {
+                uint64_t R[2][4];
+                const int64_t E[2] = {o_cross + es, o_swap + es};
+                raw_quads<2>(ph, E, avail, R);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    crossed &= ~((uint32_t)(R[0][k] >> 63) << k);
+                    negate |= (uint32_t)(1u - (uint32_t)(R[1][k] >> 63)) << k;
+                }
+            }
+            const int nq = __popc(crossed);
+            int incl = nq;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(~0u, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(~0u, incl, 31);
+            {
+                uint64_t R[1][4];
+                const int64_t E[1] = {o_mu + es};
+                raw_quads<1>(ph, E, avail, R);
+                int slot = incl - nq;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if ((crossed >> k) & 1) {
+                        s_mu[warp][slot] = u01(R[0][k]);
+                        s_g[warp][slot] = (int32_t)(gs + k) | (int32_t)(((negate >> k) & 1) << 30);
+                        ++slot;
+                    }
+            }
+            uint32_t hit = 0;
+            {
+                uint64_t R[2][4];
+                const int64_t E[2] = {o_hit + es, o_hit + hd + es};  // (second unused in single mode)
+                raw_quads<2>(ph, E, avail, R);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    hit |= (uint32_t)(((okm >> k) & 1) && (int64_t)(R[0][k] >> 11) <= pm_thr) << k;
+                    if (!single) hit |= (uint32_t)(((okm >> k) & 1) && (int64_t)(R[1][k] >> 11) <= pm_thr) << (4 + k);
+                }
+            }
+            if (j0 + lane < QP) flags[q * QP + j0 + lane] = (uint16_t)(crossed | hit << 4);
+            __syncwarp();
+            for (int t = lane; t < total; t += 32) {
+                const int32_t gw = s_g[warp][t];
+                const double b0 = sbx_beta(s_mu[warp][t], e);
+                bq[gw & 0x3FFFFFFF] = (SWAP && (gw >> 30)) ? -b0 : b0;  // beta * (1 - 2 [swap])
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(temo_problem P, VarArgs V,
+                                                                const double *__restrict__ X,
+                                                                const int64_t *__restrict__ i1,
+                                                                const int64_t *__restrict__ i2, int64_t h,
+                                                                Philox ph, uint64_t off, int swap,
+                                                                const double *__restrict__ beta,
+                                                                const uint16_t *__restrict__ flags,
+                                                                double *__restrict__ O,
+                                                                double *__restrict__ FO, int single) {
+    extern __shared__ double ssm[];
+    const int64_t d = P.d;
+    double *s_lo = ssm, *s_hi = ssm + d, *s_cf = ssm + 2 * d;
+    signed char *s_grp = reinterpret_cast<signed char *>(ssm + 3 * d);
+    const bool lsmop = P.id == TEMO_PROB_LSMOP1;
+    for (int64_t g = threadIdx.x; g < d; g += blockDim.x) {
+        s_lo[g] = V.lower[g];
+        s_hi[g] = V.upper[g];
+        s_cf[g] = 1.0 + (double)(g + 1) / (double)d;
+        int grp = -1;
+        const int64_t rel = g - (M - 1);
+        if (lsmop) {
+            for (int i = 0; i < M; ++i)
+                if (rel >= P.offset[i] && rel < P.offset[i + 1]) grp = i;
+        } else if (rel >= 0) {
+            grp = 0;
+        }
+        s_grp[g] = (signed char)grp;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t hd = h * d;
+    const int64_t o_mu = (int64_t)off;
+    const int64_t o_pmu = o_mu + (swap ? 3 * hd : hd);
+    const int64_t avail = 4 - ph.pos;
+    const double eta = V.eta_m + 1.0;
+    const int64_t QP = quads_per_pair(d);
+    for (int64_t q = (int64_t)blockIdx.x * RW + (threadIdx.x >> 5); q < h; q += (int64_t)gridDim.x * RW) {
+        const double *x1 = X + i1[q] * d;
+        const double *x2 = X + i2[q] * d;
+        const double *bq = beta + q * d;
+        double *o1 = O + q * d;
+        double *o2 = O + (h + q) * d;
+        const int sh = (int)((o_mu + q * d - avail) & 3);
+        double part1[M], part2[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) part1[i] = part2[i] = 0.0;
+        double x0a = 0.0, x0b = 0.0;
+        for (int64_t base = -sh, j0 = 0; base < d; base += 128, j0 += 32) {
+            const int64_t gs = base + 4 * lane;
+            const int64_t es = q * d + gs;
+            const uint32_t fl = (j0 + lane < QP) ? flags[q * QP + j0 + lane] : 0u;
+            const uint32_t crossed = fl & 0xF, hit = (fl >> 4) & 0xFF;
+            double c1[4], c2[4];
+            bool ok[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t g = gs + k;
+                ok[k] = g >= 0 && g < d;
+                const double a = ok[k] ? __ldg(x1 + g) : 0.0;
+                const double b = ok[k] ? __ldg(x2 + g) : 0.0;
+                double y1 = a, y2 = b;
+                if ((crossed >> k) & 1) {
+                    const double shift = 0.5 * (1.0 - __ldg(bq + g));
+                    y1 = a + shift * (b - a);
+                    y2 = b + shift * (a - b);
+                }
+                if (ok[k]) {
+                    y1 = clipv(y1, s_lo[g], s_hi[g]);
+                    y2 = clipv(y2, s_lo[g], s_hi[g]);
+                }
+                c1[k] = y1;
+                c2[k] = y2;
+            }
+            if (hit) {  // polynomial mutation (variation.py:104-120), only where hit
+                uint64_t m1[4], m2[4];
+                if (hit & 0xF) raw_quad(ph, o_pmu + es, avail, m1);
+                if (hit & 0xF0) raw_quad(ph, o_pmu + hd + es, avail, m2);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t g = gs + k;
+                    if ((hit >> k) & 1)
+                        c1[k] = clipv(pm_step(c1[k], s_lo[g], s_hi[g], u01(m1[k]), eta), s_lo[g], s_hi[g]);
+                    if ((hit >> (4 + k)) & 1)
+                        c2[k] = clipv(pm_step(c2[k], s_lo[g], s_hi[g], u01(m2[k]), eta), s_lo[g], s_hi[g]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (ok[k]) {
+                    o1[gs + k] = c1[k];
+                    if (!single) o2[gs + k] = c2[k];
+                }
+            if (!FO) continue;
+            if (base == -sh) {
+                x0a = __shfl_sync(~0u, pick4(c1, sh), 0);
+                x0b = __shfl_sync(~0u, pick4(c2, sh), 0);
+            }
+            if (lsmop) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int grp = ok[k] ? (int)s_grp[gs + k] : -1;
+                    if (grp < 0) continue;
+                    const double cf = s_cf[gs + k];
+                    const double xa = cf * c1[k] - 10.0 * x0a;
+                    const double sa = xa * xa;
+                    const double xb = cf * c2[k] - 10.0 * x0b;
+                    const double sb = xb * xb;
+#pragma unroll
+                    for (int i = 0; i < M; ++i)
+                        if (grp == i) {
+                            part1[i] += sa;
+                            if (!single) part2[i] += sb;
+                        }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (ok[k]) {
+                        acc_gene<M>(P, gs + k, c1[k], x0a, part1);
+                        if (!single) acc_gene<M>(P, gs + k, c2[k], x0b, part2);
+                    }
+            }
+        }
+        if (!FO) continue;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int s = 16; s; s >>= 1) {
+                part1[i] += __shfl_xor_sync(~0u, part1[i], s);
+                part2[i] += __shfl_xor_sync(~0u, part2[i], s);
+            }
+        __syncwarp();
+        if (lane == 0) {
+            double f[M];
+            finish_objs<M>(P, o1, part1, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[q * M + i] = f[i];
+        } else if (lane == 1 && !single) {
+            double f[M];
+            finish_objs<M>(P, o2, part2, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[(h + q) * M + i] = f[i];
+        }
+    }
+}
+
 // ------------------------------------------------------------------ standalone operators
 __global__ void k_sbx(VarArgs V, const double *__restrict__ X1, const double *__restrict__ X2,
                       int64_t q, int64_t d, Philox ph, USrc umu, USrc usw, USrc ucr,
@@ -1151,6 +1397,54 @@ static int launch_offspring(const temo_problem *prob, const temo_variation *var,
         break;
     TEMO_M_SWITCH(prob->m, OFF_CASE)
 #undef OFF_CASE
+    TEMO_LAUNCH_CHECK();
+    stage_end(S_OFFSPRING, s);
+    return TEMO_OK;
+}
+
+extern "C" size_t temo_offspring_ws_bytes(int64_t h, int64_t d) {
+    if (h < 0 || d < 1) return 0;
+    return (size_t)round_up((int64_t)(h * d * sizeof(double)), 256) +
+           (size_t)(h * quads_per_pair(d) * sizeof(uint16_t)) + 256;
+}
+
+extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const double *X,
+                                 const int64_t *i1, const int64_t *i2, int64_t h,
+                                 const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                                 void *ws, size_t ws_bytes, temo_stream_t stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !st || !O) return TEMO_EINVAL;
+    if (h == 0) return TEMO_OK;
+    const int64_t d = prob->d;
+    // two-phase path needs congruent streams (one Philox block per quad) and staged constants
+    if ((h * d) % 4 != 0 || d > SMAX_D)
+        return launch_offspring(prob, var, X, i1, i2, h, st, off, O, FO, 0, s);
+    if (!ws || ws_bytes < temo_offspring_ws_bytes(h, d)) return TEMO_EWORKSPACE;
+    double *beta = static_cast<double *>(ws);
+    uint16_t *flags = reinterpret_cast<uint16_t *>(static_cast<char *>(ws) + round_up((int64_t)(h * d * sizeof(double)), 256));
+    const Philox ph = philox_from(*st);
+    const VarArgs V = var_args(var);
+    const int64_t want = (h + RW - 1) / RW;
+    stage_begin(S_OFFSPRING, s);
+    {
+        const unsigned grid = (unsigned)(want < num_sms() * 4 * 8 ? want : num_sms() * 4 * 8);
+        if (var->gene_swap)
+            k_offspring_rand<true><<<grid, RW * 32, 0, s>>>(d, V, h, ph, off, 0, beta, flags);
+        else
+            k_offspring_rand<false><<<grid, RW * 32, 0, s>>>(d, V, h, ph, off, 0, beta, flags);
+    }
+    const size_t sm_a = 3 * d * sizeof(double) + d + 16;
+    const unsigned grid = (unsigned)(want < num_sms() * 3 * 8 ? want : num_sms() * 3 * 8);
+#define APPLY_CASE(MM)                                                                              \
+    case MM:                                                                                        \
+        if (sm_a > 48 * 1024)                                                                       \
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)sm_a));                                             \
+        k_offspring_apply<MM><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off, var->gene_swap, \
+                                                         beta, flags, O, FO, 0);                    \
+        break;
+    TEMO_M_SWITCH(prob->m, APPLY_CASE)
+#undef APPLY_CASE
     TEMO_LAUNCH_CHECK();
     stage_end(S_OFFSPRING, s);
     return TEMO_OK;

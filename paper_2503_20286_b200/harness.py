@@ -131,6 +131,9 @@ class _Stepper:
                                 t.empty((self.N, m), dtype=t.float64, device=self.dev))
         self.bufs = (mk(), mk())
         self.i12 = t.empty(2 * self.h, dtype=t.int64, device=self.dev)
+        # two-phase offspring workspace (h x d SBX betas + per-quad flags), owned by the stepper
+        self.off_ws = t.empty(max(int(_lib.lib().temo_offspring_ws_bytes(self.h, d)), 256),
+                              dtype=t.uint8, device=self.dev)
         self.perm = t.empty(self.N, dtype=t.int64, device=self.dev)
         alg = config.algorithm
         if alg == "nsga3":
@@ -186,10 +189,11 @@ class _Stepper:
         hd = self.h * self.spec.d
         off = draws.take((3 if self.params.gene_swap else 1) * hd + 4 * hd)
         cur = st.cur
-        rc = _lib.lib().temo_offspring(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
-                                       _lib.ptr(self.i12), _lib.ptr(self.i12[self.h:]), self.h,
-                                       _lib.sptr(draws.state), off, _lib.ptr(cur.X[self.n:]),
-                                       _lib.ptr(cur.F[self.n:]), _lib.stream_handle(self.dev))
+        rc = _lib.lib().temo_offspring_ws(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
+                                          _lib.ptr(self.i12), _lib.ptr(self.i12[self.h:]), self.h,
+                                          _lib.sptr(draws.state), off, _lib.ptr(cur.X[self.n:]),
+                                          _lib.ptr(cur.F[self.n:]), _lib.ptr(self.off_ws), self.off_ws.numel(),
+                                          _lib.stream_handle(self.dev))
         _lib.check(rc, "offspring")
         draws.commit()
 

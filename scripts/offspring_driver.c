@@ -13,6 +13,7 @@ int main(int argc, char **argv) {
     long long n = argc > 1 ? atoll(argv[1]) : 200000;
     long long d = argc > 2 ? atoll(argv[2]) : 1000;
     int reps = argc > 3 ? atoi(argv[3]) : 2;
+    int use_ws = argc > 4 && argv[4][0] == 'w';  /* "ws": two-phase temo_offspring_ws */
     const int m = 3;
     long long h = n / 2;
     double *hX = (double *)malloc(sizeof(double) * n * d);
@@ -55,11 +56,16 @@ int main(int argc, char **argv) {
     temo_philox_state st;
     memset(&st, 0, sizeof(st));
     st.key[0] = 0x1234; st.key[1] = 0x5678; st.buffer_pos = 4;
+    size_t ws_bytes = temo_offspring_ws_bytes(h, d);
+    void *ws = NULL;
+    cudaMalloc(&ws, ws_bytes);
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
     for (int r = 0; r < reps; ++r) {
         cudaEventRecord(a, 0);
-        int rc = temo_offspring(&P, &V, X, (const int64_t *)idx, (const int64_t *)(idx + h), h, &st, 0, O, FO, 0);
+        int rc = use_ws ? temo_offspring_ws(&P, &V, X, (const int64_t *)idx, (const int64_t *)(idx + h), h, &st, 0,
+                                            O, FO, ws, ws_bytes, 0)
+                        : temo_offspring(&P, &V, X, (const int64_t *)idx, (const int64_t *)(idx + h), h, &st, 0, O, FO, 0);
         cudaEventRecord(b, 0);
         cudaEventSynchronize(b);
         float ms = 0;

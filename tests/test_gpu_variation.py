@@ -142,7 +142,8 @@ def test_fused_offspring_matches_oracle(cuda, name, m, d, n):
 def test_sbx_beta_fast_vs_numpy(cuda):
     """The exp/log SBX spread factor used by the fused offspring kernel (csrc/sbx_pow.cuh)
     against np.power on the reference's expression (variation.py:77-78): 10^6 Philox draws
-    plus the edge cases of the U grid.  Bound: 1.5e-15 relative (a few ulp; the offspring
+    plus the edge cases of the U grid.  Bound: 4e-15 relative (the exp/log form loses about
+    |e log(base)| ulp, up to 24 at eta_c = 0.5 and U = 2^-53; the offspring
     parity tests need 1e-13)."""
     import torch
 
@@ -164,4 +165,47 @@ def test_sbx_beta_fast_vs_numpy(cuda):
             got = out.cpu().numpy()
             rel = np.abs(got - want) / np.where(want == 0, 1.0, want)
             assert got[0] == 0.0 and np.all(np.isfinite(got))
-            assert rel.max() < 1.5e-15, (eta_c, fast, rel.max())
+            assert rel.max() < 4e-15, (eta_c, fast, rel.max())
+
+
+@pytest.mark.parametrize("name,m,d,h,pre", [("lsmop1", 3, 1000, 40, 0), ("lsmop1", 3, 1000, 40, 3),
+                                            ("dtlz1", 3, 12, 50, 1), ("dtlz2", 5, 40, 16, 2),
+                                            ("dtlz7", 3, 13, 3, 0)])
+def test_offspring_two_phase_equals_fused(cuda, name, m, d, h, pre):
+    """temo_offspring_ws (randomness kernel + streaming apply kernel, the harness path) is
+    bit-identical to the fused temo_offspring for every stream alignment (``pre`` shifts the
+    host Generator's buffered words) and falls back to the fused kernel when h*d % 4 != 0."""
+    import torch
+
+    from paper_2503_20286_b200 import _lib
+    from paper_2503_20286_b200.problems import make_problem
+    from paper_2503_20286_b200.rng import DeviceDraws
+    from paper_2503_20286_b200.variation import VariationParams
+
+    spec = make_problem(name, m=m, d=d)
+    dev = torch.device("cuda", 0)
+    var = VariationParams(lower=spec.lower, upper=spec.upper).struct(d, dev)
+    prob = spec.struct()
+    gen = philox_gen(7)
+    gen.random(pre)
+    X = torch.from_numpy(spec.lower + np.random.default_rng(1).random((2 * h, d)) * (spec.upper - spec.lower)).to(dev)
+    idx = torch.from_numpy(np.random.default_rng(2).permutation(2 * h).astype(np.int64)).to(dev)
+    draws = DeviceDraws(gen)
+    off = draws.take(7 * h * d)
+    outs = []
+    for two_phase in (False, True):
+        O = torch.full((2 * h, d), np.nan, dtype=torch.float64, device=dev)
+        FO = torch.full((2 * h, m), np.nan, dtype=torch.float64, device=dev)
+        L, s = _lib.lib(), _lib.stream_handle(dev)
+        args = (_lib.sptr(prob), _lib.sptr(var), _lib.ptr(X), _lib.ptr(idx), _lib.ptr(idx[h:]), h,
+                _lib.sptr(draws.state), off, _lib.ptr(O), _lib.ptr(FO))
+        if two_phase:
+            ws = torch.empty(max(L.temo_offspring_ws_bytes(h, d), 256), dtype=torch.uint8, device=dev)
+            rc = L.temo_offspring_ws(*args, _lib.ptr(ws), ws.numel(), s)
+        else:
+            rc = L.temo_offspring(*args, s)
+        assert rc == 0
+        outs.append((O.cpu().numpy(), FO.cpu().numpy()))
+    (O1, F1), (O2, F2) = outs
+    assert not np.isnan(O1).any() and not np.isnan(F1).any()
+    assert np.array_equal(O1, O2) and np.array_equal(F1, F2)
