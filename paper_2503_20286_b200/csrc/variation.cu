@@ -935,6 +935,9 @@ __global__ void __launch_bounds__(SW * 32, OFF_S_MINB) k_offspring_s(temo_proble
 // high occupancy for the serial Philox and pow chains.
 // Phase 2 `k_offspring_apply`: parents, flags and betas in, children and
 // objectives out (PM's rare mu draws on the spot) -- a streaming kernel.
+#ifndef OFF_APPLY_PREFETCH
+#define OFF_APPLY_PREFETCH 0
+#endif
 #ifndef OFF_APPLY_MINB
 #define OFF_APPLY_MINB 2
 #endif
@@ -948,7 +951,6 @@ __global__ void __launch_bounds__(RW * 32, 4) k_offspring_rand(int64_t d, VarArg
                                                                double *__restrict__ beta,
                                                                uint16_t *__restrict__ flags) {
     __shared__ double s_mu[RW][128];
-    __shared__ int32_t s_g[RW][128];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t hd = h * d;
     const int64_t o_mu = (int64_t)off, o_swap = o_mu + hd, o_cross = o_mu + (SWAP ? 2 * hd : 0);
@@ -995,11 +997,7 @@ __global__ void __launch_bounds__(RW * 32, 4) k_offspring_rand(int64_t d, VarArg
                 int slot = incl - nq;
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if ((crossed >> k) & 1) {
-                        s_mu[warp][slot] = u01(R[0][k]);
-                        s_g[warp][slot] = (int32_t)(gs + k) | (int32_t)(((negate >> k) & 1) << 30);
-                        ++slot;
-                    }
+                    if ((crossed >> k) & 1) s_mu[warp][slot++] = u01(R[0][k]);
             }
             uint32_t hit = 0;
             {
@@ -1014,17 +1012,28 @@ __global__ void __launch_bounds__(RW * 32, 4) k_offspring_rand(int64_t d, VarArg
             }
             if (j0 + lane < QP) flags[q * QP + j0 + lane] = (uint16_t)(crossed | hit << 4);
             __syncwarp();
-            for (int t = lane; t < total; t += 32) {
-                const int32_t gw = s_g[warp][t];
-                const double b0 = sbx_beta(s_mu[warp][t], e);
-                bq[gw & 0x3FFFFFFF] = (SWAP && (gw >> 30)) ? -b0 : b0;  // beta * (1 - 2 [swap])
+            for (int t = lane; t < total; t += 32) s_mu[warp][t] = sbx_beta(s_mu[warp][t], e);
+            __syncwarp();
+            // the owner lane writes its quad's 4 betas (uncrossed: 1), so every 32-byte sector
+            // of the beta array is written whole (scattered 8-byte writes cost a DRAM read-modify-write)
+            {
+                int slot = incl - nq;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    double b = 1.0;
+                    if ((crossed >> k) & 1) {
+                        b = s_mu[warp][slot++];
+                        if (SWAP && ((negate >> k) & 1)) b = -b;  // beta * (1 - 2 [swap])
+                    }
+                    if ((okm >> k) & 1) bq[gs + k] = b;
+                }
             }
             __syncwarp();
         }
     }
 }
 
-template <int M>
+template <int M, bool LSMOP>
 __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(temo_problem P, VarArgs V,
                                                                 const double *__restrict__ X,
                                                                 const int64_t *__restrict__ i1,
@@ -1038,7 +1047,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
     const int64_t d = P.d;
     double *s_lo = ssm, *s_hi = ssm + d, *s_cf = ssm + 2 * d;
     signed char *s_grp = reinterpret_cast<signed char *>(ssm + 3 * d);
-    const bool lsmop = P.id == TEMO_PROB_LSMOP1;
+    constexpr bool lsmop = LSMOP;
     for (int64_t g = threadIdx.x; g < d; g += blockDim.x) {
         s_lo[g] = V.lower[g];
         s_hi[g] = V.upper[g];
@@ -1075,6 +1084,16 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
         for (int64_t base = -sh, j0 = 0; base < d; base += 128, j0 += 32) {
             const int64_t gs = base + 4 * lane;
             const int64_t es = q * d + gs;
+#if OFF_APPLY_PREFETCH
+            {  // next round's parent and beta quads into L1 (no registers held)
+                const int64_t gn = gs + 128;
+                if (gn < d) {
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(x1 + gn));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(x2 + gn));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(bq + gn));
+                }
+            }
+#endif
             const uint32_t fl = (j0 + lane < QP) ? flags[q * QP + j0 + lane] : 0u;
             const uint32_t crossed = fl & 0xF, hit = (fl >> 4) & 0xFF;
             double c1[4], c2[4];
@@ -1122,7 +1141,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
                 x0a = __shfl_sync(~0u, pick4(c1, sh), 0);
                 x0b = __shfl_sync(~0u, pick4(c2, sh), 0);
             }
-            if (lsmop) {
+            if constexpr (LSMOP) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int grp = ok[k] ? (int)s_grp[gs + k] : -1;
@@ -1437,11 +1456,18 @@ extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation 
     const unsigned grid = (unsigned)(want < num_sms() * 3 * 8 ? want : num_sms() * 3 * 8);
 #define APPLY_CASE(MM)                                                                              \
     case MM:                                                                                        \
-        if (sm_a > 48 * 1024)                                                                       \
-            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           (int)sm_a));                                             \
-        k_offspring_apply<MM><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off, var->gene_swap, \
-                                                         beta, flags, O, FO, 0);                    \
+        if (sm_a > 48 * 1024) {                                                                     \
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<MM, true>,                             \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a)); \
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<MM, false>,                            \
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a)); \
+        }                                                                                           \
+        if (prob->id == TEMO_PROB_LSMOP1)                                                           \
+            k_offspring_apply<MM, true><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off,  \
+                                                                   var->gene_swap, beta, flags, O, FO, 0); \
+        else                                                                                        \
+            k_offspring_apply<MM, false><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off, \
+                                                                    var->gene_swap, beta, flags, O, FO, 0); \
         break;
     TEMO_M_SWITCH(prob->m, APPLY_CASE)
 #undef APPLY_CASE
