@@ -333,7 +333,7 @@ def our_arm(args):
     t0 = time.perf_counter()
     for g in range(args.steps):
         st, _ = stepper.step(st, g, gen)
-        F_host[g % 2].copy_(stepper.population(st)[1], non_blocking=True)
+        F_host[g % 2].copy_(stepper.objectives(st), non_blocking=True)
         done[g % 2].record()
         if g > 0:
             done[(g - 1) % 2].synchronize()

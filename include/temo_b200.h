@@ -218,13 +218,24 @@ int temo_offspring(const temo_problem *prob, const temo_variation *var, const do
 /* Same result as temo_offspring, computed in two phases through caller workspace
  * (temo_offspring_ws_bytes(h, d) bytes: h*d betas + per-quad flags): a pure-randomness
  * kernel (Philox draws, SBX betas of crossed genes, PM hit bits) and a streaming apply
- * kernel (parents -> children -> objectives).  Falls back to the fused kernel when the
- * streams are not congruent mod 4 or d is above the staged-constant limit. */
+ * kernel (parents -> children -> objectives).  Row pool (both NULL = plain layout):
+ * parent i is row src_map[i] of X, child r (r < 2h) goes to row dst_rows[r] of O.
+ * Falls back to the fused kernel when the streams are not congruent mod 4 or d is
+ * above the staged-constant limit (row maps are then rejected with TEMO_EINVAL). */
 size_t temo_offspring_ws_bytes(int64_t h, int64_t d);
 int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const double *X,
                       const int64_t *i1, const int64_t *i2, int64_t h, const temo_philox_state *st,
-                      uint64_t off, double *O, double *FO, void *ws, size_t ws_bytes,
-                      temo_stream_t stream);
+                      uint64_t off, double *O, double *FO, const int64_t *src_map,
+                      const int64_t *dst_rows, void *ws, size_t ws_bytes, temo_stream_t stream);
+
+/* Row-pool bookkeeping after a selection (replaces the survivor row copy X[perm][keep] of
+ * nsga3.py:218 / hype.py:163): phys (N) maps logical merged rows to pool rows; the n
+ * survivors are logical rows perm[keep[p]] (perm NULL = identity).  phys_out[p] =
+ * phys[perm[keep[p]]] for p < n, and phys_out[n..N) = the other pool rows in logical
+ * order (the free rows the next offspring overwrite).  ws: temo_pool_update_ws_bytes(N). */
+size_t temo_pool_update_ws_bytes(int64_t N);
+int temo_pool_update(const int64_t *phys, const int64_t *perm, const int32_t *keep, int64_t N, int64_t n,
+                     int64_t *phys_out, void *ws, size_t ws_bytes, temo_stream_t stream);
 
 /* ------------------------------------------------------------------ MOEA/D
  * temo_moead_offspring: moead.moead_offspring (moead.py:127-145) for parents

@@ -994,6 +994,55 @@ extern "C" int temo_gather_rows(const double *src, const int32_t *idx32, const i
     return TEMO_OK;
 }
 
+// ---------------------------------------------------------------- row pool
+__global__ void k_pool_survivors(const int64_t *__restrict__ phys, const int64_t *__restrict__ perm,
+                                 const int32_t *__restrict__ keep, int64_t n, int64_t *__restrict__ out,
+                                 int32_t *__restrict__ kept) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int64_t r = perm ? perm[keep[p]] : (int64_t)keep[p];
+    out[p] = phys[r];
+    kept[r] = 1;
+}
+
+__global__ void k_pool_free_flags(const int32_t *__restrict__ kept, int64_t N, int32_t *__restrict__ fr) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < N) fr[r] = 1 - kept[r];
+}
+
+__global__ void k_pool_free(const int64_t *__restrict__ phys, const int32_t *__restrict__ kept,
+                            const int32_t *__restrict__ pos, int64_t N, int64_t n, int64_t *__restrict__ out) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < N && !kept[r]) out[n + pos[r]] = phys[r];
+}
+
+extern "C" size_t temo_pool_update_ws_bytes(int64_t N) {
+    if (N < 1) return 0;
+    size_t c = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, c, (int32_t *)nullptr, (int32_t *)nullptr, (int)N);
+    return 3 * ((size_t)N * 4 + 256) + c + 256;
+}
+
+extern "C" int temo_pool_update(const int64_t *phys, const int64_t *perm, const int32_t *keep, int64_t N,
+                                int64_t n, int64_t *phys_out, void *ws, size_t ws_bytes,
+                                temo_stream_t stream) {
+    if (N < 1 || n < 0 || n > N || !phys || !keep || !phys_out || phys_out == phys) return TEMO_EINVAL;
+    if (!ws || ws_bytes < temo_pool_update_ws_bytes(N)) return TEMO_EWORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    Carve c(ws);
+    int32_t *kept = c.take<int32_t>(N), *fr = c.take<int32_t>(N), *pos = c.take<int32_t>(N);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, fr, pos, (int)N);
+    void *tmp = c.take<char>(tb);
+    TEMO_CUDA(cudaMemsetAsync(kept, 0, sizeof(int32_t) * N, st));
+    if (n) k_pool_survivors<<<g1(n), NT, 0, st>>>(phys, perm, keep, n, phys_out, kept);
+    k_pool_free_flags<<<g1(N), NT, 0, st>>>(kept, N, fr);
+    TEMO_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, fr, pos, (int)N, st));
+    k_pool_free<<<g1(N), NT, 0, st>>>(phys, kept, pos, N, n, phys_out);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
 extern "C" int temo_gather_rows2(const double *src, const int64_t *idx_a, const int32_t *idx_b,
                                  int64_t rows, int64_t cols, double *dst, temo_stream_t stream) {
     if (rows < 0 || cols < 1 || !idx_a || !idx_b) return TEMO_EINVAL;

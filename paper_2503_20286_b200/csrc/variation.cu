@@ -1042,7 +1042,9 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
                                                                 const double *__restrict__ beta,
                                                                 const uint16_t *__restrict__ flags,
                                                                 double *__restrict__ O,
-                                                                double *__restrict__ FO, int single) {
+                                                                double *__restrict__ FO, int single,
+                                                                const int64_t *__restrict__ src_map,
+                                                                const int64_t *__restrict__ dst_rows) {
     extern __shared__ double ssm[];
     const int64_t d = P.d;
     double *s_lo = ssm, *s_hi = ssm + d, *s_cf = ssm + 2 * d;
@@ -1071,11 +1073,14 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
     const double eta = V.eta_m + 1.0;
     const int64_t QP = quads_per_pair(d);
     for (int64_t q = (int64_t)blockIdx.x * RW + (threadIdx.x >> 5); q < h; q += (int64_t)gridDim.x * RW) {
-        const double *x1 = X + i1[q] * d;
-        const double *x2 = X + i2[q] * d;
+        // row pool (harness): parents at physical rows src_map[i], children into rows dst_rows[r]
+        const int64_t p1 = src_map ? src_map[i1[q]] : i1[q];
+        const int64_t p2 = src_map ? src_map[i2[q]] : i2[q];
+        const double *x1 = X + p1 * d;
+        const double *x2 = X + p2 * d;
         const double *bq = beta + q * d;
-        double *o1 = O + q * d;
-        double *o2 = O + (h + q) * d;
+        double *o1 = O + (dst_rows ? dst_rows[q] : q) * d;
+        double *o2 = O + (dst_rows ? dst_rows[h + q] : h + q) * d;
         const int sh = (int)((o_mu + q * d - avail) & 3);
         double part1[M], part2[M];
 #pragma unroll
@@ -1430,14 +1435,17 @@ extern "C" size_t temo_offspring_ws_bytes(int64_t h, int64_t d) {
 extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const double *X,
                                  const int64_t *i1, const int64_t *i2, int64_t h,
                                  const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                                 const int64_t *src_map, const int64_t *dst_rows,
                                  void *ws, size_t ws_bytes, temo_stream_t stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !st || !O) return TEMO_EINVAL;
     if (h == 0) return TEMO_OK;
     const int64_t d = prob->d;
     // two-phase path needs congruent streams (one Philox block per quad) and staged constants
-    if ((h * d) % 4 != 0 || d > SMAX_D)
+    if ((h * d) % 4 != 0 || d > SMAX_D) {
+        if (src_map || dst_rows) return TEMO_EINVAL;  // row maps only on the two-phase path
         return launch_offspring(prob, var, X, i1, i2, h, st, off, O, FO, 0, s);
+    }
     if (!ws || ws_bytes < temo_offspring_ws_bytes(h, d)) return TEMO_EWORKSPACE;
     double *beta = static_cast<double *>(ws);
     uint16_t *flags = reinterpret_cast<uint16_t *>(static_cast<char *>(ws) + round_up((int64_t)(h * d * sizeof(double)), 256));
@@ -1464,10 +1472,12 @@ extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation 
         }                                                                                           \
         if (prob->id == TEMO_PROB_LSMOP1)                                                           \
             k_offspring_apply<MM, true><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off,  \
-                                                                   var->gene_swap, beta, flags, O, FO, 0); \
+                                                                   var->gene_swap, beta, flags, O, FO, 0,  \
+                                                                   src_map, dst_rows);              \
         else                                                                                        \
             k_offspring_apply<MM, false><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off, \
-                                                                    var->gene_swap, beta, flags, O, FO, 0); \
+                                                                    var->gene_swap, beta, flags, O, FO, 0, \
+                                                                    src_map, dst_rows);             \
         break;
     TEMO_M_SWITCH(prob->m, APPLY_CASE)
 #undef APPLY_CASE

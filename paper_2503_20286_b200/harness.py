@@ -6,9 +6,14 @@
 run's NumPy Generator, every uniform block is produced on the device from the
 same Philox stream, and the population never leaves HBM.
 
-Merged populations use a fixed buffer: parents occupy rows [0, n) and the
-offspring rows [n, n + 2h), the reference's [X; O] order (harness.py:221-222).
-Survivors are gathered into a second buffer (ping-pong).
+Decision variables live in ONE row pool of N = n + 2h rows (no survivor
+copy): ``phys`` (device int64, N) maps the logical merged order -- parents
+[0, n), offspring [n, N), the reference's [X; O] order (harness.py:221-222) --
+to pool rows.  The offspring kernel reads parents through ``phys`` and writes
+children into the pool rows ``phys[n:]``; after selection ``temo_pool_update``
+rewrites ``phys`` (survivors first, freed rows after), so X[perm][keep]
+(nsga3.py:218) is a 3.2 GB copy the generation never makes.  Objectives are
+small and stay in logical order (ping-pong buffers).
 """
 
 from __future__ import annotations
@@ -96,16 +101,23 @@ class PopBuffers:
 
 @dataclass
 class DeviceState:
-    """Current population: rows [0, n) of ``cur``; ``nxt`` receives survivors."""
+    """Current population: logical rows [0, n); X rows live in the pool at ``phys``."""
 
     cur: PopBuffers
     nxt: PopBuffers
     n: int
     extra: dict = field(default_factory=dict)
+    phys: object = None  # device int64 (N): logical merged row -> pool row (None: identity)
+
+    def rows(self, lo: int, hi: int):
+        """X of logical rows [lo, hi) (materialised from the pool)."""
+        if self.phys is None:
+            return self.cur.X[lo:hi]
+        return self.cur.X.index_select(0, self.phys[lo:hi])
 
     @property
     def X(self):
-        return self.cur.X[: self.n]
+        return self.rows(0, self.n)
 
     @property
     def F(self):
@@ -127,9 +139,13 @@ class _Stepper:
         self.N = n + 2 * self.h
         self.ring = _lib.HostRing()
         d, m = spec.d, spec.m
-        mk = lambda: PopBuffers(t.empty((self.N, d), dtype=t.float64, device=self.dev),  # noqa: E731
-                                t.empty((self.N, m), dtype=t.float64, device=self.dev))
+        pool = t.empty((self.N, d), dtype=t.float64, device=self.dev)  # the single X row pool
+        mk = lambda: PopBuffers(pool, t.empty((self.N, m), dtype=t.float64, device=self.dev))  # noqa: E731
         self.bufs = (mk(), mk())
+        self.phys = [t.arange(self.N, dtype=t.int64, device=self.dev),
+                     t.empty(self.N, dtype=t.int64, device=self.dev)]
+        self.pool_ws = t.empty(max(int(_lib.lib().temo_pool_update_ws_bytes(self.N)), 256),
+                               dtype=t.uint8, device=self.dev)
         self.i12 = t.empty(2 * self.h, dtype=t.int64, device=self.dev)
         # two-phase offspring workspace (h x d SBX betas + per-quad flags), owned by the stepper
         self.off_ws = t.empty(max(int(_lib.lib().temo_offspring_ws_bytes(self.h, d)), 256),
@@ -177,6 +193,9 @@ class _Stepper:
 
         evaluate_device(self.spec, cur.X[: self.n], out=cur.F[: self.n])
         st = DeviceState(cur, self.bufs[1], self.n)
+        if self.config.algorithm != "moead":
+            st.phys = self.phys[0]  # identity at init: parents in pool rows [0, n)
+            st.extra["pool_identity"] = True
         if self.config.algorithm == "moead":
             st.extra["moead"] = self.engine.init_state(cur.X[: self.n], cur.F[: self.n])
         return st
@@ -189,13 +208,43 @@ class _Stepper:
         hd = self.h * self.spec.d
         off = draws.take((3 if self.params.gene_swap else 1) * hd + 4 * hd)
         cur = st.cur
+        pooled = ((self.h * self.spec.d) % 4 == 0 and self.spec.d <= 3000  # two-phase path (row maps)
+                  and not getattr(self, "force_unpooled", False))
+        if pooled:
+            src, dst, obase = _lib.ptr(st.phys), _lib.ptr(st.phys[self.n:]), _lib.ptr(cur.X)
+        else:  # fused fallback: children into logical rows; make the pool the identity first
+            self._pool_identity(st)
+            src, dst, obase = None, None, _lib.ptr(cur.X[self.n:])
         rc = _lib.lib().temo_offspring_ws(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
                                           _lib.ptr(self.i12), _lib.ptr(self.i12[self.h:]), self.h,
-                                          _lib.sptr(draws.state), off, _lib.ptr(cur.X[self.n:]),
-                                          _lib.ptr(cur.F[self.n:]), _lib.ptr(self.off_ws), self.off_ws.numel(),
+                                          _lib.sptr(draws.state), off, obase,
+                                          _lib.ptr(cur.F[self.n:]), src, dst,
+                                          _lib.ptr(self.off_ws), self.off_ws.numel(),
                                           _lib.stream_handle(self.dev))
         _lib.check(rc, "offspring")
         draws.commit()
+
+    def _pool_identity(self, st: DeviceState):
+        """Materialise the parents into pool rows [0, n) (fused-offspring fallback only)."""
+        if st.phys is not None and st.extra.get("pool_identity") is not True:
+            X = st.rows(0, self.n)
+            st.cur.X[: self.n].copy_(X)
+            st.phys.copy_(_lib.torch().arange(self.N, dtype=_lib.torch().int64, device=self.dev))
+        st.extra["pool_identity"] = True
+
+    def _pool_update(self, st: DeviceState, perm, keep):
+        """phys' = survivors' pool rows, then the freed rows (temo_pool_update)."""
+        out = self.phys[1] if st.phys.data_ptr() == self.phys[0].data_ptr() else self.phys[0]
+        rc = _lib.lib().temo_pool_update(_lib.ptr(st.phys), _lib.ptr(perm), _lib.ptr(keep), self.N, self.n,
+                                         _lib.ptr(out), _lib.ptr(self.pool_ws), self.pool_ws.numel(),
+                                         _lib.stream_handle(self.dev))
+        _lib.check(rc, "pool_update")
+        st.phys = out
+        st.extra["pool_identity"] = False
+
+    def offspring_rows(self, st: DeviceState):
+        """X of the current offspring (logical rows [n, N))."""
+        return st.rows(self.n, self.N)
 
     def step(self, st: DeviceState, g: int, gen):
         alg = self.config.algorithm
@@ -210,14 +259,20 @@ class _Stepper:
         if alg == "nsga3":
             self.ring.upload(np.asarray(gen.permutation(self.N), dtype=np.int64), self.perm)
             keep = self.selector.select(cur.F, self.perm)
-            _lib.gather_rows2(cur.X, self.perm, keep, nxt.X[:n])
+            self._pool_update(st, self.perm, keep)  # survivors' X rows stay where they are
             _lib.gather_rows(self.selector.Fs, keep, nxt.F[:n])
         else:  # hype (no shuffle; hype.py:135-163)
             keep = self.selector.select(cur.F, gen)
-            _lib.gather_rows(cur.X, keep, nxt.X[:n])
+            self._pool_update(st, None, keep)
             _lib.gather_rows(cur.F, keep, nxt.F[:n])
         st.cur, st.nxt = nxt, cur
         return st, time.perf_counter() - ts
+
+    def objectives(self, st: DeviceState):
+        """F of the current population (device, logical order) -- no X materialisation."""
+        if self.config.algorithm == "moead":
+            return st.extra["moead"].F1
+        return st.F
 
     def population(self, st: DeviceState):
         if self.config.algorithm == "moead":
@@ -255,11 +310,11 @@ def run(config: RunConfig, sync_every_step: bool = True) -> RunRecord:
     for g in range(1, config.generations + 1):
         t0 = time.perf_counter()
         st, sel_s = stepper.step(st, g, gen)
-        _, F = stepper.population(st)
+        F = stepper.objectives(st)
         ideal = F.min(dim=0).values.cpu().numpy().tolist() if sync_every_step else []
         total = time.perf_counter() - t0
         rows.append(GenRow(g, sel_s if config.time_selection_only else total, ideal))
-    _, F = stepper.population(st)
+    F = stepper.objectives(st)
     Fh = F.cpu().numpy()
     mean = float(np.mean([r.time_s for r in rows])) if rows else math.nan
     return RunRecord(dataclasses.asdict(config), rows, mean, Fh)

@@ -132,7 +132,7 @@ def test_fused_offspring_matches_oracle(cuda, name, m, d, n):
     torch.cuda.synchronize()
     O_ref = ovar.offspring(g_ref, X0, 20.0, 20.0, None, spec.lower, spec.upper)
     h = n // 2
-    O = state.cur.X[n:n + 2 * h].cpu().numpy()
+    O = st_.offspring_rows(state).cpu().numpy()
     assert np.allclose(O, O_ref, rtol=1e-13, atol=1e-13)
     FO = state.cur.F[n:n + 2 * h].cpu().numpy()
     assert np.allclose(FO, oprob.evaluate(name, O_ref, m), rtol=1e-10, atol=1e-12)
@@ -201,7 +201,7 @@ def test_offspring_two_phase_equals_fused(cuda, name, m, d, h, pre):
                 _lib.sptr(draws.state), off, _lib.ptr(O), _lib.ptr(FO))
         if two_phase:
             ws = torch.empty(max(L.temo_offspring_ws_bytes(h, d), 256), dtype=torch.uint8, device=dev)
-            rc = L.temo_offspring_ws(*args, _lib.ptr(ws), ws.numel(), s)
+            rc = L.temo_offspring_ws(*args, None, None, _lib.ptr(ws), ws.numel(), s)
         else:
             rc = L.temo_offspring(*args, s)
         assert rc == 0
@@ -209,3 +209,46 @@ def test_offspring_two_phase_equals_fused(cuda, name, m, d, h, pre):
     (O1, F1), (O2, F2) = outs
     assert not np.isnan(O1).any() and not np.isnan(F1).any()
     assert np.array_equal(O1, O2) and np.array_equal(F1, F2)
+
+
+@pytest.mark.parametrize("alg", ["nsga3", "hype"])
+def test_row_pool_equals_survivor_copy(cuda, alg):
+    """The harness keeps X in one row pool (temo_pool_update instead of the X[perm][keep]
+    copy of nsga3.py:218 / hype.py:163).  Over several generations the pooled population
+    equals (1) a torch restatement that materialises [X; O][perm][keep] every step and
+    (2) the unpooled path (fused offspring kernel writing contiguous rows), bit for bit."""
+    import torch
+
+    from paper_2503_20286_b200.directions import das_dennis
+    from paper_2503_20286_b200.harness import RunConfig, _Stepper
+    from paper_2503_20286_b200.problems import make_problem
+
+    name, m, d, n = "dtlz2", 3, 40, 64
+    spec = make_problem(name, m=m, d=d)
+    cfg = RunConfig(algorithm=alg, problem=name, objectives=m, dim=d, pop_size=n, hv_samples=4000)
+    runs = []
+    for unpooled in (False, True):
+        st_ = _Stepper(cfg, spec, das_dennis(m, 6), n)
+        st_.force_unpooled = unpooled
+        captured = []
+        orig = st_._offspring
+
+        def offspring_and_capture(state, gen, orig=orig, st_=st_, captured=captured):
+            orig(state, gen)
+            captured.append(st_.offspring_rows(state).clone())
+
+        st_._offspring = offspring_and_capture
+        gen = philox_gen(11)
+        state = st_.init(gen)
+        X_ref = state.X.clone()
+        traj = []
+        for g in range(4):
+            state, _ = st_.step(state, g, gen)
+            merged = torch.cat([X_ref, captured[-1]])
+            keep = st_.selector.keep.long()
+            X_ref = merged[st_.perm][keep] if alg == "nsga3" else merged[keep]
+            assert torch.equal(state.X, X_ref), (unpooled, g)
+            traj.append((state.X.cpu().numpy(), state.F.cpu().numpy()))
+        runs.append(traj)
+    for (Xa, Fa), (Xb, Fb) in zip(*runs):
+        assert np.array_equal(Xa, Xb) and np.array_equal(Fa, Fb)
