@@ -216,7 +216,7 @@ def k1_traffic(N):
     exists for this N (profiles/traffic.json), else None."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        return t.get("k_dom_packed", {}).get(str(N))
+        return t.get("k_dom_rows8", {}).get(str(N))
     except Exception:
         return None
 
@@ -225,7 +225,7 @@ def k1_roofline_hbm(N, m, ws, avg_s):
     peak, src = hbm_peak()
     b = k1_bytes(N, ws)
     ach = b / avg_s / 1e9
-    return {"bound": "hbm", "kernel": "k_dom_packed (K1 dominance bitmap)", "achieved": ach, "peak": peak,
+    return {"bound": "hbm", "kernel": "k_dom_rows8 (K1 dominance bitmap)", "achieved": ach, "peak": peak,
             "unit": "GB/s", "frac": ach / peak, "traffic": k1_traffic(N), "algorithmic_bytes": b,
             "avg_launch_ms": avg_s * 1e3, "peak_source": src,
             "note": "K1 is integer-issue bound, not HBM bound (see roofline_compute); bytes = bitmap "
@@ -240,7 +240,7 @@ def k1_roofline_int(N, m, ws, avg_s, sm_mhz):
     ops_per_pair = (m - 1 + (m - 1 + 1) // 2 + 1) / 2
     peak = 148 * 128 * sm_mhz * 1e6 / ops_per_pair
     ach = pairs / avg_s
-    return {"bound": "int-issue", "kernel": "k_dom_packed", "achieved": ach / 1e12, "peak": peak / 1e12,
+    return {"bound": "int-issue", "kernel": "k_dom_rows8", "achieved": ach / 1e12, "peak": peak / 1e12,
             "unit": "Tpair/s", "frac": ach / peak, "work_per_launch": pairs,
             "lane_ops_per_pair": ops_per_pair, "sm_mhz": sm_mhz}
 

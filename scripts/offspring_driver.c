@@ -64,7 +64,7 @@ int main(int argc, char **argv) {
     for (int r = 0; r < reps; ++r) {
         cudaEventRecord(a, 0);
         int rc = use_ws ? temo_offspring_ws(&P, &V, X, (const int64_t *)idx, (const int64_t *)(idx + h), h, &st, 0,
-                                            O, FO, ws, ws_bytes, 0)
+                                            O, FO, NULL, NULL, ws, ws_bytes, 0)
                         : temo_offspring(&P, &V, X, (const int64_t *)idx, (const int64_t *)(idx + h), h, &st, 0, O, FO, 0);
         cudaEventRecord(b, 0);
         cudaEventSynchronize(b);
