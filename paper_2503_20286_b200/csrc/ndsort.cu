@@ -872,14 +872,16 @@ __global__ void __launch_bounds__(K1W * 32, K1_R8_MINB) k_dom_rows8(const uint4 
                             if (r2 == r) acc[r2] = __brev(~a);
                     }
                 }
-                // masks: rows past N, columns past N
-                uint32_t cm = ~0u;
-                if (tail < TILE) {
-                    const int64_t base = 32 * jw;
-                    if (tail < base + 32) cm = tail <= base ? 0u : (1u << (tail - base)) - 1u;
-                }
+                // masks: rows past N, columns past N (only the last row/column tiles need them)
+                if (tail < TILE || row_ok != 0xFFu) {
+                    uint32_t cm = ~0u;
+                    if (tail < TILE) {
+                        const int64_t base = 32 * jw;
+                        if (tail < base + 32) cm = tail <= base ? 0u : (1u << (tail - base)) - 1u;
+                    }
 #pragma unroll
-                for (int r = 0; r < RPL; ++r) acc[r] &= ((row_ok >> r) & 1) ? cm : 0u;
+                    for (int r = 0; r < RPL; ++r) acc[r] &= ((row_ok >> r) & 1) ? cm : 0u;
+                }
 #pragma unroll
                 for (int r = 0; r < RPL; ++r) sw[32 * 9 * r + jw] = acc[r];
                 // column counts over the warp's 256 rows: bit-sliced sum of 8 rows, 4 transposes
