@@ -321,10 +321,11 @@ def our_arm(args):
 
     # ---- end-to-end through the public harness API: every step uploads its host inputs
     # (the host RNG's pairing + shuffle permutations, pinned ring) and reads its objective
-    # matrix back to pinned host memory.  One step in flight: the host draws step g+1's
-    # permutations while the GPU runs step g; step g's result is waited for right after.
-    F_host = [torch.empty((n, spec.m), dtype=torch.float64).pin_memory() for _ in range(2)]
-    done = [torch.cuda.Event(), torch.cuda.Event()]
+    # matrix back to pinned host memory.  Up to LAG steps in flight: the host draws the next
+    # steps' permutations while the GPU runs; step g's result is waited for LAG steps later.
+    LAG = 2
+    F_host = [torch.empty((n, spec.m), dtype=torch.float64).pin_memory() for _ in range(LAG + 1)]
+    done = [torch.cuda.Event() for _ in range(LAG + 1)]
     h = n // 2
     h2d = 8 * (2 * h + (n + 2 * h))  # pairing permutation + shuffle permutation (int64)
     d2h = F_host[0].numel() * 8
@@ -333,13 +334,14 @@ def our_arm(args):
     t0 = time.perf_counter()
     for g in range(args.steps):
         st, _ = stepper.step(st, g, gen)
-        F_host[g % 2].copy_(stepper.objectives(st), non_blocking=True)
-        done[g % 2].record()
-        if g > 0:
-            done[(g - 1) % 2].synchronize()
-            checksum += float(F_host[(g - 1) % 2][0, 0])
-    done[(args.steps - 1) % 2].synchronize()
-    checksum += float(F_host[(args.steps - 1) % 2][0, 0])
+        F_host[g % (LAG + 1)].copy_(stepper.objectives(st), non_blocking=True)
+        done[g % (LAG + 1)].record()
+        if g >= LAG:
+            done[(g - LAG) % (LAG + 1)].synchronize()
+            checksum += float(F_host[(g - LAG) % (LAG + 1)][0, 0])
+    for g in range(max(args.steps - LAG, 0), args.steps):
+        done[g % (LAG + 1)].synchronize()
+        checksum += float(F_host[g % (LAG + 1)][0, 0])
     barrier()
     e2e_s = time.perf_counter() - t0
     t_e2e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
