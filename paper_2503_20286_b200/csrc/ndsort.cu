@@ -28,8 +28,13 @@ namespace temo {
 constexpr int TILE = 256;        // K1 tile edge (rows i and columns j)
 constexpr int CHUNK = 8;         // K1: row tiles per work item
 constexpr int PEEL_T = 256;      // K2 threads per CTA
-constexpr int ROWS_PER_WARP = 30;
-constexpr int LC = 8 * ROWS_PER_WARP;  // K2: list rows per work item (<= 255 per byte counter)
+constexpr int ROWS_PER_WARP = 30;       // K2 (shard path): list rows per warp per work item
+constexpr int LC = 8 * ROWS_PER_WARP;    // K2 (shard path): list rows per work item (<= 255 per byte)
+#ifndef PEEL_HALVES
+#define PEEL_HALVES 2
+#endif
+constexpr int PEEL_RPW = 30 * PEEL_HALVES;  // K2: rows per warp per item, resolved 30 at a time (<= 255)
+constexpr int PEEL_LC = 8 * PEEL_RPW;       // K2: rows per item (cross-warp sums unpacked to int)
 constexpr int MAX_M = 16;
 
 int num_sms() {
@@ -976,42 +981,44 @@ __device__ void vertical_pass(const PeelArgs &a, const int *rows_below, const in
         }
         const int wb = lo;
         const int chunk = item - item_pref[wb];
-        const int r0 = chunk * LC + warp * ROWS_PER_WARP;
-        const int r1 = min(r0 + ROWS_PER_WARP, rows_below[wb]);
+        const int rw0 = chunk * PEEL_LC + warp * PEEL_RPW;
+        const int rw1 = min(rw0 + PEEL_RPW, rows_below[wb]);
         const int64_t w = (int64_t)wb * 32 + lane;
-        // lane k resolves row r0+k once (list entry, row base address, first stored
-        // word); the row loop then only shuffles and issues independent loads
-        const int rr = max(r1 - r0, 0);
-        int64_t my_base = 0;
-        int my_w0 = 0x7FFFFFFF;
-        if (lane < rr) {
-            const int i = identity ? r0 + lane : a.list[r0 + lane];
-            const int64_t it = i >> 8;
-            my_base = a.rt_off[it] + (int64_t)(i & 255) * (a.W - 8 * it) - 8 * it;
-            my_w0 = (int)(8 * it);
-        }
         uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0, o0 = 0, o1 = 0, o2 = 0, o3 = 0;
-        for (int g = 0; g < rr; g += 15) {
-            uint32_t xs[15];
-#pragma unroll
-            for (int q = 0; q < 15; ++q) {
-                const int64_t b = __shfl_sync(~0u, my_base, (g + q) & 31);
-                const int w0 = __shfl_sync(~0u, my_w0, (g + q) & 31);
-                xs[q] = (g + q < rr && w >= w0) ? __ldg(a.bits + b + w) : 0u;
+        for (int r0 = rw0; r0 < rw1; r0 += 30) {  // 30 rows per round: one row per lane
+            const int rr = min(30, rw1 - r0);
+            // lane k resolves row r0+k once (list entry, row base address, first stored
+            // word); the row loop then only shuffles and issues independent loads
+            int64_t my_base = 0;
+            int my_w0 = 0x7FFFFFFF;
+            if (lane < rr) {
+                const int i = identity ? r0 + lane : a.list[r0 + lane];
+                const int64_t it = i >> 8;
+                my_base = a.rt_off[it] + (int64_t)(i & 255) * (a.W - 8 * it) - 8 * it;
+                my_w0 = (int)(8 * it);
             }
-            uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            for (int g = 0; g < rr; g += 15) {
+                uint32_t xs[15];
 #pragma unroll
-            for (int q = 0; q < 15; ++q) {
-                const uint32_t x = xs[q];
-                a0 += x & 0x11111111u;
-                a1 += (x >> 1) & 0x11111111u;
-                a2 += (x >> 2) & 0x11111111u;
-                a3 += (x >> 3) & 0x11111111u;
+                for (int q = 0; q < 15; ++q) {
+                    const int64_t b = __shfl_sync(~0u, my_base, (g + q) & 31);
+                    const int w0 = __shfl_sync(~0u, my_w0, (g + q) & 31);
+                    xs[q] = (g + q < rr && w >= w0) ? __ldg(a.bits + b + w) : 0u;
+                }
+                uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+                for (int q = 0; q < 15; ++q) {
+                    const uint32_t x = xs[q];
+                    a0 += x & 0x11111111u;
+                    a1 += (x >> 1) & 0x11111111u;
+                    a2 += (x >> 2) & 0x11111111u;
+                    a3 += (x >> 3) & 0x11111111u;
+                }
+                e0 += a0 & 0x0F0F0F0Fu; o0 += (a0 >> 4) & 0x0F0F0F0Fu;
+                e1 += a1 & 0x0F0F0F0Fu; o1 += (a1 >> 4) & 0x0F0F0F0Fu;
+                e2 += a2 & 0x0F0F0F0Fu; o2 += (a2 >> 4) & 0x0F0F0F0Fu;
+                e3 += a3 & 0x0F0F0F0Fu; o3 += (a3 >> 4) & 0x0F0F0F0Fu;
             }
-            e0 += a0 & 0x0F0F0F0Fu; o0 += (a0 >> 4) & 0x0F0F0F0Fu;
-            e1 += a1 & 0x0F0F0F0Fu; o1 += (a1 >> 4) & 0x0F0F0F0Fu;
-            e2 += a2 & 0x0F0F0F0Fu; o2 += (a2 >> 4) & 0x0F0F0F0Fu;
-            e3 += a3 & 0x0F0F0F0Fu; o3 += (a3 >> 4) & 0x0F0F0F0Fu;
         }
         uint32_t *mine = sred + warp * 8 * 32 + lane;
         mine[0 * 32] = e0; mine[1 * 32] = e1; mine[2 * 32] = e2; mine[3 * 32] = e3;
@@ -1019,14 +1026,18 @@ __device__ void vertical_pass(const PeelArgs &a, const int *rows_below, const in
         __syncthreads();
         {
             const int q = tid >> 5, l = tid & 31;  // q: which byte register, l: word column
-            uint32_t s = 0;
+            int sb[4] = {0, 0, 0, 0};  // per-byte sums over the 8 warps (each byte <= ROWS_PER_WARP)
 #pragma unroll
-            for (int ww = 0; ww < 8; ++ww) s += sred[(ww * 8 + q) * 32 + l];
+            for (int ww = 0; ww < 8; ++ww) {
+                const uint32_t v = sred[(ww * 8 + q) * 32 + l];
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) sb[nb] += (v >> (8 * nb)) & 255;
+            }
             const int64_t col = ((int64_t)wb * 32 + l) * 32;
             const int kk = q & 3, half = q >> 2;
 #pragma unroll
             for (int nb = 0; nb < 4; ++nb) {
-                const int c = (s >> (8 * nb)) & 255;
+                const int c = sb[nb];
                 if (c) atomicAdd(a.cnt + col + 8 * nb + 4 * half + kk, sign * c);
             }
         }
@@ -1102,7 +1113,7 @@ __global__ void __launch_bounds__(PEEL_T) k_peel(PeelArgs a) {
         // B: subtract the front's bits.  s_rows holds exclusive starts with
         // s_rows[NB] = total, so rows_below(wb) = s_rows[wb + 1].
         for (int wb = tid; wb <= a.NB; wb += PEEL_T)
-            s_items[wb] = wb < a.NB ? (s_rows[wb + 1] + LC - 1) / LC : 0;
+            s_items[wb] = wb < a.NB ? (s_rows[wb + 1] + PEEL_LC - 1) / PEEL_LC : 0;
         __syncthreads();
         block_exclusive_scan(s_items, a.NB + 1, s_tmp);
         vertical_pass(a, s_rows + 1, s_items, false, -1, sred);

@@ -226,14 +226,18 @@ __global__ void __launch_bounds__(PEEL_T) k_shard_subtract(
         __syncthreads();
         {
             const int q = tid >> 5, l = tid & 31;
-            uint32_t sum = 0;
+            int sb[4] = {0, 0, 0, 0};  // per-byte sums over the 8 warps (each byte <= ROWS_PER_WARP)
 #pragma unroll
-            for (int ww = 0; ww < 8; ++ww) sum += sred[(ww * 8 + q) * 32 + l];
+            for (int ww = 0; ww < 8; ++ww) {
+                const uint32_t v = sred[(ww * 8 + q) * 32 + l];
+#pragma unroll
+                for (int nbyte = 0; nbyte < 4; ++nbyte) sb[nbyte] += (v >> (8 * nbyte)) & 255;
+            }
             const int64_t col = (wb * 32 + l) * 32 - (int64_t)TILE * jt_lo;  // local column
             const int kk = q & 3, half = q >> 2;
 #pragma unroll
             for (int nbyte = 0; nbyte < 4; ++nbyte) {
-                const int c = (sum >> (8 * nbyte)) & 255;
+                const int c = sb[nbyte];
                 if (c) atomicSub(cnt + col + 8 * nbyte + 4 * half + kk, c);
             }
         }
