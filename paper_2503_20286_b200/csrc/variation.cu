@@ -938,6 +938,9 @@ __global__ void __launch_bounds__(SW * 32, OFF_S_MINB) k_offspring_s(temo_proble
 #ifndef OFF_APPLY_PREFETCH
 #define OFF_APPLY_PREFETCH 0
 #endif
+#ifndef OFF_RAND_MINB
+#define OFF_RAND_MINB 4
+#endif
 #ifndef OFF_APPLY_MINB
 #define OFF_APPLY_MINB 2
 #endif
@@ -946,7 +949,7 @@ constexpr int RW = 8;  // warps per CTA of both phases
 __host__ __device__ inline int64_t quads_per_pair(int64_t d) { return (d + 3) / 4 + 1; }
 
 template <bool SWAP>
-__global__ void __launch_bounds__(RW * 32, 4) k_offspring_rand(int64_t d, VarArgs V, int64_t h, Philox ph,
+__global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64_t d, VarArgs V, int64_t h, Philox ph,
                                                                uint64_t off, int single,
                                                                double *__restrict__ beta,
                                                                uint16_t *__restrict__ flags) {
