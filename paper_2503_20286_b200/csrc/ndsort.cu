@@ -37,6 +37,7 @@ constexpr int PEEL_RPW = 30 * PEEL_HALVES;  // K2: rows per warp per item, resol
 constexpr int PEEL_LC = 8 * PEEL_RPW;       // K2: rows per item (cross-warp sums unpacked to int)
 constexpr int MAX_M = 16;
 
+#ifndef TEMO_M_ONLY
 int num_sms() {
     static int sms = 0;
     if (!sms) {
@@ -47,6 +48,7 @@ int num_sms() {
     }
     return sms;
 }
+#endif
 
 // ------------------------------------------------------------------ plan
 struct RankPlan {
@@ -126,6 +128,7 @@ static void plan_rank(RankPlan &p, void *base, int64_t N, int m) {
     p.total = c.off;
 }
 
+#ifndef TEMO_M_ONLY  // non-template kernels: base translation unit only
 // ------------------------------------------------------------------ K0
 __global__ void k_col_keys(const double *__restrict__ F, int64_t N, int m, int col,
                            uint64_t *__restrict__ keys, int32_t *__restrict__ vals,
@@ -207,6 +210,8 @@ __global__ void k_rowtile_offsets(int64_t nT, int64_t W, int64_t *off, int64_t *
     lo[I] = 8 * I;
     stride[I] = W - 8 * I;
 }
+
+#endif  // TEMO_M_ONLY
 
 // ------------------------------------------------------------------ K1
 __device__ __forceinline__ uint32_t fld(const uint4 *r, int k) {
@@ -919,6 +924,90 @@ __global__ void __launch_bounds__(K1W * 32, K1_R8_MINB) k_dom_rows8(const uint4 
     }
 }
 
+// ------------------------------------------------------ per-M K1 launchers
+// build.py compiles this file as a base unit plus one unit per objective count
+// (-DTEMO_M_ONLY=M), each instantiating only its dom_m<M>.
+// TEMO_K1_UNPACKED=1 selects the per-column sign-bit kernel (A/B comparisons)
+static bool packed_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_K1_UNPACKED");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+// TEMO_K1_ROWS8=0 selects the 1-row-per-lane packed kernel (A/B comparisons)
+static bool rows8_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_K1_ROWS8");
+        v = (e && e[0] == '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+template <int M>
+int dom_m(const RankPlan &p, const BitLayout &L, uint32_t *bits, int32_t *cnt, cudaStream_t st) {
+    const uint4 *rec = p.rec;
+    const int64_t N = p.N, nT = p.nT;
+    if constexpr (M >= 2) {
+        if (!packed_disabled()) {
+            const int64_t K = (nT + SUPER_TILES - 1) / SUPER_TILES;
+            dim3 g;
+            if (L.grid2d) {
+                const int64_t T0 = L.jt_lo / SUPER_TILES, T1 = (L.jt_hi + SUPER_TILES - 1) / SUPER_TILES;
+                g = dim3((unsigned)(T1 - T0), (unsigned)L.jt_hi);
+            } else {
+                g = dim3((unsigned)(SUPER_TILES * (K * (K + 1) / 2)));
+            }
+            TEMO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * TILE * (L.jt_hi - L.jt_lo), st));
+            k_local_ranks<M - 1><<<dim3((unsigned)K, M - 1), 256, 0, st>>>(rec, p.Np, p.lsorted, p.qpk);
+            if (M <= 5 && !rows8_disabled()) {
+                dim3 g8;
+                if (L.grid2d) {
+                    const int64_t T0 = L.jt_lo / SUPER_TILES, T1 = (L.jt_hi + SUPER_TILES - 1) / SUPER_TILES;
+                    g8 = dim3((unsigned)(T1 - T0), (unsigned)((L.jt_hi + K1W - 1) / K1W));
+                } else {
+                    g8 = dim3((unsigned)(K * (K + 1)));
+                }
+                if (rows8_smem(M) > 48 * 1024)
+                    TEMO_CUDA(cudaFuncSetAttribute(k_dom_rows8<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)rows8_smem(M)));
+                k_dom_rows8<M><<<g8, K1W * 32, rows8_smem(M), st>>>(rec, p.qpk, p.lsorted, N, nT, L, bits, cnt);
+                return TEMO_OK;
+            }
+            if (packed_smem(M) > 48 * 1024)
+                TEMO_CUDA(cudaFuncSetAttribute(k_dom_packed<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)packed_smem(M)));
+            k_dom_packed<M><<<g, TILE, packed_smem(M), st>>>(rec, p.qpk, p.lsorted, N, nT, L, bits, cnt);
+            return TEMO_OK;
+        }
+    }
+    dim3 g;
+    if (L.grid2d) {
+        g = dim3((unsigned)((L.jt_hi - L.jt_lo + CHUNK - 1) / CHUNK), (unsigned)L.jt_hi);
+    } else {
+        g = dim3((unsigned)(nT + CHUNK * ((nT / CHUNK) * ((nT / CHUNK) - 1) / 2) + (nT % CHUNK) * (nT / CHUNK)));
+    }
+    TEMO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * TILE * (L.jt_hi - L.jt_lo), st));
+    k_dom_rows<M><<<g, TILE, 0, st>>>(rec, N, nT, L, bits, cnt);
+    return TEMO_OK;
+}
+
+#define TEMO_ND_M_LIST(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+#define TEMO_ND_DECL(MM, EXT) \
+    EXT template int dom_m<MM>(const RankPlan &, const BitLayout &, uint32_t *, int32_t *, cudaStream_t);
+#ifdef TEMO_M_ONLY
+TEMO_ND_DECL(TEMO_M_ONLY, )
+}  // namespace temo
+#else
+#define TEMO_ND_EXTERN(MM) TEMO_ND_DECL(MM, extern)
+TEMO_ND_EXTERN(2) TEMO_ND_EXTERN(3) TEMO_ND_EXTERN(4) TEMO_ND_EXTERN(5) TEMO_ND_EXTERN(6) TEMO_ND_EXTERN(7)
+TEMO_ND_EXTERN(8) TEMO_ND_EXTERN(9) TEMO_ND_EXTERN(10) TEMO_ND_EXTERN(11) TEMO_ND_EXTERN(12)
+TEMO_ND_EXTERN(13) TEMO_ND_EXTERN(14) TEMO_ND_EXTERN(15) TEMO_ND_EXTERN(16)
+TEMO_ND_DECL(1, )  // m = 1 (per-column path only) lives in the base unit
+
 // ------------------------------------------------------------------ K2
 struct PeelArgs {
     const uint32_t *bits;
@@ -1167,26 +1256,6 @@ __global__ void k_inverse(const int32_t *__restrict__ order, int64_t N, int32_t 
 }
 
 // ------------------------------------------------------------------ host
-// TEMO_K1_UNPACKED=1 selects the per-column sign-bit kernel (A/B comparisons)
-static bool packed_disabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("TEMO_K1_UNPACKED");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
-// TEMO_K1_ROWS8=0 selects the 1-row-per-lane packed kernel (A/B comparisons)
-static bool rows8_disabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("TEMO_K1_ROWS8");
-        v = (e && e[0] == '0') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 static inline dim3 grid1(int64_t n, int t = 256) { return dim3((unsigned)((n + t - 1) / t)); }
 
 // K0: column ranks, lex order (p.vals_a), run ids and records (p.rec)
@@ -1231,72 +1300,18 @@ static int build_records(RankPlan &p, const double *F, int32_t *status, cudaStre
     return TEMO_OK;
 }
 
-// K1 over the column tiles of `L`; cnt (zeroed here) is indexed from column tile L.jt_lo
+// K1 over the column tiles of `L`; cnt (zeroed in dom_m) is indexed from column tile L.jt_lo
 static int launch_dom(const RankPlan &p, const BitLayout &L, uint32_t *bits, int32_t *cnt,
                       cudaStream_t st) {
-    const int m = p.m;
-    const uint4 *rec = p.rec;
-    const int64_t N = p.N, nT = p.nT;
     stage_begin(S_DOM_BITS, st);
-    if (m >= 2 && !packed_disabled()) {
-        const int64_t K = (nT + SUPER_TILES - 1) / SUPER_TILES;
-        dim3 g;
-        if (L.grid2d) {
-            const int64_t T0 = L.jt_lo / SUPER_TILES, T1 = (L.jt_hi + SUPER_TILES - 1) / SUPER_TILES;
-            g = dim3((unsigned)(T1 - T0), (unsigned)L.jt_hi);
-        } else {
-            g = dim3((unsigned)(SUPER_TILES * (K * (K + 1) / 2)));
-        }
-        TEMO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * TILE * (L.jt_hi - L.jt_lo), st));
-#define PACK_CASE(MM)                                                                              \
-    case MM:                                                                                       \
-        k_local_ranks<MM - 1><<<dim3((unsigned)K, MM - 1), 256, 0, st>>>(rec, p.Np, p.lsorted, p.qpk); \
-        if (MM <= 5 && !rows8_disabled()) {                                                        \
-            dim3 g8;                                                                               \
-            if (L.grid2d) {                                                                        \
-                const int64_t T0 = L.jt_lo / SUPER_TILES, T1 = (L.jt_hi + SUPER_TILES - 1) / SUPER_TILES; \
-                g8 = dim3((unsigned)(T1 - T0), (unsigned)((L.jt_hi + K1W - 1) / K1W));              \
-            } else {                                                                               \
-                g8 = dim3((unsigned)(K * (K + 1)));                                                \
-            }                                                                                      \
-            if (rows8_smem(MM) > 48 * 1024)                                                        \
-                TEMO_CUDA(cudaFuncSetAttribute(k_dom_rows8<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                               (int)rows8_smem(MM)));                              \
-            k_dom_rows8<MM><<<g8, K1W * 32, rows8_smem(MM), st>>>(rec, p.qpk, p.lsorted, N, nT, L, bits, cnt); \
-            break;                                                                                 \
-        }                                                                                          \
-        if (packed_smem(MM) > 48 * 1024)                                                           \
-            TEMO_CUDA(cudaFuncSetAttribute(k_dom_packed<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           (int)packed_smem(MM)));                                   \
-        k_dom_packed<MM><<<g, TILE, packed_smem(MM), st>>>(rec, p.qpk, p.lsorted, N, nT, L, bits, cnt); \
-        break;
-        switch (m) {
-            PACK_CASE(2) PACK_CASE(3) PACK_CASE(4) PACK_CASE(5) PACK_CASE(6) PACK_CASE(7) PACK_CASE(8)
-            PACK_CASE(9) PACK_CASE(10) PACK_CASE(11) PACK_CASE(12) PACK_CASE(13) PACK_CASE(14)
-            PACK_CASE(15) PACK_CASE(16)
-            default: return TEMO_EINVAL;
-        }
-#undef PACK_CASE
-        TEMO_LAUNCH_CHECK();
-        stage_end(S_DOM_BITS, st);
-        return TEMO_OK;
-    }
-    dim3 g;
-    if (L.grid2d) {
-        g = dim3((unsigned)((L.jt_hi - L.jt_lo + CHUNK - 1) / CHUNK), (unsigned)L.jt_hi);
-    } else {
-        g = dim3((unsigned)(nT + CHUNK * ((nT / CHUNK) * ((nT / CHUNK) - 1) / 2) + (nT % CHUNK) * (nT / CHUNK)));
-    }
-    TEMO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * TILE * (L.jt_hi - L.jt_lo), st));
-#define DOM_CASE(MM) \
-    case MM: k_dom_rows<MM><<<g, TILE, 0, st>>>(rec, N, nT, L, bits, cnt); break;
-    switch (m) {
-        DOM_CASE(1) DOM_CASE(2) DOM_CASE(3) DOM_CASE(4) DOM_CASE(5) DOM_CASE(6) DOM_CASE(7)
-        DOM_CASE(8) DOM_CASE(9) DOM_CASE(10) DOM_CASE(11) DOM_CASE(12) DOM_CASE(13) DOM_CASE(14)
-        DOM_CASE(15) DOM_CASE(16)
+    int rc = TEMO_EINVAL;
+#define DOM_CASE(MM) case MM: rc = dom_m<MM>(p, L, bits, cnt, st); break;
+    switch (p.m) {
+        TEMO_ND_M_LIST(DOM_CASE)
         default: return TEMO_EINVAL;
     }
 #undef DOM_CASE
+    if (rc) return rc;
     TEMO_LAUNCH_CHECK();
     stage_end(S_DOM_BITS, st);
     return TEMO_OK;
@@ -1398,3 +1413,5 @@ extern "C" int temo_dominance(const double *F, int64_t N, int m, uint32_t *D_out
 }
 
 #include "ndsort_shard.cuh"
+
+#endif  // TEMO_M_ONLY

@@ -43,7 +43,7 @@ __device__ __forceinline__ void sbx_gene(double x1, double x2, double mu, double
     c2 = x2 + shift * (x1 - x2);
 }
 
-__device__ __noinline__ double pm_step(double x, double lo, double hi, double mu, double eta) {
+static __device__ __noinline__ double pm_step(double x, double lo, double hi, double mu, double eta) {
     const double span = hi - lo;
     double step;
     if (0.5 - mu >= 0.0) {
@@ -70,7 +70,7 @@ __device__ __forceinline__ double uniform1(const Philox &ph, uint64_t e) {
 }
 
 // ------------------------------------------------------------------ evaluation
-__device__ double block_sum(double v, double *red) {
+static __device__ double block_sum(double v, double *red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(~0u, v, d);
     __syncthreads();
@@ -702,7 +702,7 @@ constexpr int SW = 8;            // warps per CTA
 
 // SBX spread factor of one crossed gene (variation.py:77-78); out of line so pow's
 // internal registers do not inflate the register budget of the offspring kernel
-__device__ __noinline__ double sbx_beta(double mu, double e) {
+static __device__ __noinline__ double sbx_beta(double mu, double e) {
     return pow((0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu), e);
 }
 constexpr int SMAX_D = 3000;     // genes staged in shared memory (else k_offspring_w)
@@ -1198,6 +1198,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
     }
 }
 
+#ifndef TEMO_M_ONLY  // non-template kernels live in the base translation unit only
 // ------------------------------------------------------------------ standalone operators
 __global__ void k_sbx(VarArgs V, const double *__restrict__ X1, const double *__restrict__ X2,
                       int64_t q, int64_t d, Philox ph, USrc umu, USrc usw, USrc ucr,
@@ -1251,6 +1252,8 @@ __global__ void k_init_population(Philox ph, uint64_t off, int64_t rows, int64_t
     }
 }
 
+#endif  // TEMO_M_ONLY
+
 // TEMO_OFFSPRING_S=0 disables the persistent staged kernel (A/B comparisons)
 static bool offspring_s_disabled() {
     static int v = -1;
@@ -1302,9 +1305,94 @@ static Philox philox_or_zero(const temo_philox_state *st) {
         default: return TEMO_EINVAL;                                                               \
     }
 
+
+// ------------------------------------------------------------ per-M launchers
+// build.py compiles this file once as the base unit and once per objective
+// count with -DTEMO_M_ONLY=M; each per-M unit instantiates only its M (the
+// base unit declares them extern), so the M-templated kernels build in parallel.
+template <int M>
+int eval_m(const temo_problem *prob, const double *X, int64_t n, double *F, cudaStream_t s) {
+    k_evaluate<M><<<(unsigned)n, VT, 0, s>>>(*prob, X, n, F);
+    return TEMO_OK;
+}
+
+template <int M>
+int offspring_m(const temo_problem *prob, const temo_variation *var, const double *X,
+                const int64_t *i1, const int64_t *i2, int64_t h, const temo_philox_state *st,
+                uint64_t off, double *O, double *FO, int single, bool warp_path, size_t smem,
+                int smem_rows, cudaStream_t s) {
+    const int64_t d = prob->d;
+    if (warp_path && d <= SMAX_D && !offspring_s_disabled()) {
+        const size_t sm_s = (3 * d + SW * 128) * sizeof(double) + d + 16;
+        if (sm_s > 48 * 1024) {
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+        }
+        const int64_t want = (h + SW - 1) / SW;
+        const unsigned grid = (unsigned)(want < num_sms() * 2 * 4 ? want : num_sms() * 2 * 4);
+        if (var->gene_swap)
+            k_offspring_s<M, true><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h,
+                                                               philox_from(*st), off, O, FO, single);
+        else
+            k_offspring_s<M, false><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h,
+                                                                philox_from(*st), off, O, FO, single);
+    } else if (warp_path && var->gene_swap) {
+        k_offspring_w<M, true><<<(unsigned)((h + OW - 1) / OW), OW * 32, 0, s>>>(
+            *prob, var_args(var), X, i1, i2, h, philox_from(*st), off, O, FO, single);
+    } else if (warp_path) {
+        k_offspring_w<M, false><<<(unsigned)((h + OW - 1) / OW), OW * 32, 0, s>>>(
+            *prob, var_args(var), X, i1, i2, h, philox_from(*st), off, O, FO, single);
+    } else {
+        if (smem > 48 * 1024)
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        k_offspring<M><<<(unsigned)h, VT, smem, s>>>(*prob, var_args(var), X, i1, i2, h,
+                                                     philox_from(*st), off, O, FO, smem_rows, single);
+    }
+    return TEMO_OK;
+}
+
+template <int M>
+int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const int64_t *i1,
+            const int64_t *i2, int64_t h, const Philox &ph, uint64_t off, int gene_swap,
+            const double *beta, const uint16_t *flags, double *O, double *FO,
+            const int64_t *src_map, const int64_t *dst_rows, size_t sm_a, unsigned grid,
+            cudaStream_t s) {
+    if (sm_a > 48 * 1024) {
+        TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a));
+        TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a));
+    }
+    if (prob->id == TEMO_PROB_LSMOP1)
+        k_offspring_apply<M, true><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off, gene_swap,
+                                                              beta, flags, O, FO, 0, src_map, dst_rows);
+    else
+        k_offspring_apply<M, false><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off, gene_swap,
+                                                               beta, flags, O, FO, 0, src_map, dst_rows);
+    return TEMO_OK;
+}
+
+#define TEMO_M_LIST(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+#define TEMO_VAR_DECL(MM, EXT)                                                                      \
+    EXT template int eval_m<MM>(const temo_problem *, const double *, int64_t, double *, cudaStream_t); \
+    EXT template int offspring_m<MM>(const temo_problem *, const temo_variation *, const double *,   \
+                                     const int64_t *, const int64_t *, int64_t,                      \
+                                     const temo_philox_state *, uint64_t, double *, double *, int,    \
+                                     bool, size_t, int, cudaStream_t);                                \
+    EXT template int apply_m<MM>(const temo_problem *, const VarArgs &, const double *,              \
+                                 const int64_t *, const int64_t *, int64_t, const Philox &, uint64_t, \
+                                 int, const double *, const uint16_t *, double *, double *,           \
+                                 const int64_t *, const int64_t *, size_t, unsigned, cudaStream_t);
+#ifdef TEMO_M_ONLY
+TEMO_VAR_DECL(TEMO_M_ONLY, )
+#else
+#define TEMO_VAR_EXTERN(MM) TEMO_VAR_DECL(MM, extern)
+TEMO_M_LIST(TEMO_VAR_EXTERN)
+#endif
+
 }  // namespace temo
 
 using namespace temo;
+
+#ifndef TEMO_M_ONLY
 
 extern "C" int temo_evaluate(const temo_problem *prob, const double *X, int64_t n, double *F,
                              temo_stream_t stream) {
@@ -1312,7 +1400,7 @@ extern "C" int temo_evaluate(const temo_problem *prob, const double *X, int64_t 
     if (n == 0) return TEMO_OK;
     cudaStream_t s = (cudaStream_t)stream;
     stage_begin(S_EVALUATE, s);
-#define EVAL_CASE(MM) case MM: k_evaluate<MM><<<(unsigned)n, VT, 0, s>>>(*prob, X, n, F); break;
+#define EVAL_CASE(MM) case MM: { int rc = eval_m<MM>(prob, X, n, F, s); if (rc) return rc; } break;
     TEMO_M_SWITCH(prob->m, EVAL_CASE)
 #undef EVAL_CASE
     TEMO_LAUNCH_CHECK();
@@ -1391,37 +1479,11 @@ static int launch_offspring(const temo_problem *prob, const temo_variation *var,
     const bool warp_path = (h * d) % 4 == 0 && !offspring_cta_forced();
     stage_begin(S_OFFSPRING, s);
 #define OFF_CASE(MM)                                                                              \
-    case MM:                                                                                      \
-        if (warp_path && d <= SMAX_D && !offspring_s_disabled()) {                                \
-            const size_t sm_s = (3 * d + SW * 128) * sizeof(double) + d + 16;                    \
-            if (sm_s > 48 * 1024) {                                                               \
-                TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<MM, true>,                          \
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s)); \
-                TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<MM, false>,                         \
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s)); \
-            }                                                                                     \
-            const int64_t want = (h + SW - 1) / SW;                                               \
-            const unsigned grid = (unsigned)(want < num_sms() * 2 * 4 ? want : num_sms() * 2 * 4);\
-            if (var->gene_swap)                                                                   \
-                k_offspring_s<MM, true><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h, \
-                                                                   philox_from(*st), off, O, FO, single); \
-            else                                                                                  \
-                k_offspring_s<MM, false><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h, \
-                                                                    philox_from(*st), off, O, FO, single); \
-        } else if (warp_path && var->gene_swap)                                                   \
-            k_offspring_w<MM, true><<<(unsigned)((h + OW - 1) / OW), OW * 32, 0, s>>>(            \
-                *prob, var_args(var), X, i1, i2, h, philox_from(*st), off, O, FO, single);        \
-        else if (warp_path)                                                                       \
-            k_offspring_w<MM, false><<<(unsigned)((h + OW - 1) / OW), OW * 32, 0, s>>>(           \
-                *prob, var_args(var), X, i1, i2, h, philox_from(*st), off, O, FO, single);        \
-        else {                                                                                    \
-            if (smem > 48 * 1024)                                                                 \
-                TEMO_CUDA(cudaFuncSetAttribute(k_offspring<MM>,                                   \
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)); \
-            k_offspring<MM><<<(unsigned)h, VT, smem, s>>>(*prob, var_args(var), X, i1, i2, h,     \
-                                                          philox_from(*st), off, O, FO, smem_rows, single); \
-        }                                                                                         \
-        break;
+    case MM: {                                                                                    \
+        int rc = offspring_m<MM>(prob, var, X, i1, i2, h, st, off, O, FO, single, warp_path, smem, \
+                                 smem_rows, s);                                                   \
+        if (rc) return rc;                                                                        \
+    } break;
     TEMO_M_SWITCH(prob->m, OFF_CASE)
 #undef OFF_CASE
     TEMO_LAUNCH_CHECK();
@@ -1466,22 +1528,11 @@ extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation 
     const size_t sm_a = 3 * d * sizeof(double) + d + 16;
     const unsigned grid = (unsigned)(want < num_sms() * 3 * 8 ? want : num_sms() * 3 * 8);
 #define APPLY_CASE(MM)                                                                              \
-    case MM:                                                                                        \
-        if (sm_a > 48 * 1024) {                                                                     \
-            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<MM, true>,                             \
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a)); \
-            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<MM, false>,                            \
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a)); \
-        }                                                                                           \
-        if (prob->id == TEMO_PROB_LSMOP1)                                                           \
-            k_offspring_apply<MM, true><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off,  \
-                                                                   var->gene_swap, beta, flags, O, FO, 0,  \
-                                                                   src_map, dst_rows);              \
-        else                                                                                        \
-            k_offspring_apply<MM, false><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off, \
-                                                                    var->gene_swap, beta, flags, O, FO, 0, \
-                                                                    src_map, dst_rows);             \
-        break;
+    case MM: {                                                                                      \
+        int rc = apply_m<MM>(prob, V, X, i1, i2, h, ph, off, var->gene_swap, beta, flags, O, FO,   \
+                             src_map, dst_rows, sm_a, grid, s);                                     \
+        if (rc) return rc;                                                                          \
+    } break;
     TEMO_M_SWITCH(prob->m, APPLY_CASE)
 #undef APPLY_CASE
     TEMO_LAUNCH_CHECK();
@@ -1514,3 +1565,5 @@ extern "C" int temo_init_population(const temo_philox_state *st, uint64_t off, i
     TEMO_LAUNCH_CHECK();
     return TEMO_OK;
 }
+
+#endif  // TEMO_M_ONLY
