@@ -62,6 +62,7 @@ def cpu_sample(pop, dim, m, problem, seed=0, reps=1):
     from oracle import generation, problems as oprob
 
     if problem == "lsmop1":
+        dim = oprob.lsmop_dimension(m, dim)  # PlatEMO's D for the requested dimension
         lower, upper = oprob.lsmop_bounds(m, dim)
     else:
         lower, upper = np.zeros(dim), np.ones(dim)

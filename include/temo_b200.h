@@ -235,7 +235,9 @@ int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const
  * order (the free rows the next offspring overwrite).  ws: temo_pool_update_ws_bytes(N). */
 size_t temo_pool_update_ws_bytes(int64_t N);
 int temo_pool_update(const int64_t *phys, const int64_t *perm, const int32_t *keep, int64_t N, int64_t n,
-                     int64_t *phys_out, void *ws, size_t ws_bytes, temo_stream_t stream);
+                     int64_t *phys_out, const int32_t *status, void *ws, size_t ws_bytes,
+                     temo_stream_t stream);  /* status (nullable): selection status word; when it
+                                                is non-zero the pool is left as it is (phys' = phys) */
 
 /* ------------------------------------------------------------------ MOEA/D
  * temo_moead_offspring: moead.moead_offspring (moead.py:127-145) for parents

@@ -99,6 +99,20 @@ def lsmop_groups(m, d, nk=5):
     return sublen, offset
 
 
+def lsmop_dimension(m, d_request, nk=5):
+    """PlatEMO resets D = M - 1 + len(end) after sizing the subcomponents from the request."""
+    sublen, offset = lsmop_groups(m, d_request, nk)
+    return m - 1 + int(offset[m])
+
+
+def lsmop_groups_for(m, D, nk=5):
+    """Groups of the instance with D variables (D determines them: floors are monotone in the request)."""
+    for d0 in range(D, D + nk * m + 2):
+        if lsmop_dimension(m, d0, nk) == D:
+            return lsmop_groups(m, d0, nk)
+    raise ValueError(f"{D} is not an LSMOP dimension for m={m}")
+
+
 def lsmop_bounds(m, d):
     lower = np.zeros(d)
     upper = np.concatenate([np.ones(m - 1), np.full(d - m + 1, 10.0)])
@@ -109,7 +123,7 @@ def evaluate_lsmop1(X, m, nk=5):
     """LSMOP1: linear linkage, Sphere g on every group, linear (DTLZ1-type) front."""
     X = np.asarray(X, dtype=np.float64)
     n, d = X.shape
-    sublen, offset = lsmop_groups(m, d, nk)
+    sublen, offset = lsmop_groups_for(m, d, nk)
     idx = np.arange(m, d + 1, dtype=np.float64)  # 1-based indices of x^s
     xs = (1.0 + idx / d) * X[:, m - 1:] - 10.0 * X[:, :1]
     G = np.zeros((n, m))

@@ -685,10 +685,16 @@ __global__ void k_keep_write(const int32_t *__restrict__ fl, const int32_t *__re
                              int64_t N, int64_t n, int32_t *__restrict__ keep,
                              int32_t *__restrict__ scal, int32_t *status) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int kept = N ? pos[N - 1] + fl[N - 1] : 0;
     if (i == 0) {
-        const int kept = N ? pos[N - 1] + fl[N - 1] : 0;
         scal[4] = kept;
         if (kept != n) flag_status(status, TEMO_ST_COUNT);
+    }
+    // a failed selection (NaN objectives, peel/fill/count errors; the host raises on the
+    // status word) still leaves keep a valid index set, so no consumer reads garbage rows
+    if ((status && *status != 0) || kept != n) {
+        if (i < n) keep[i] = (int32_t)i;
+        return;
     }
     if (i < N && fl[i] && pos[i] < n) keep[pos[i]] = (int32_t)i;
 }
@@ -997,10 +1003,11 @@ extern "C" int temo_gather_rows(const double *src, const int32_t *idx32, const i
 // ---------------------------------------------------------------- row pool
 __global__ void k_pool_survivors(const int64_t *__restrict__ phys, const int64_t *__restrict__ perm,
                                  const int32_t *__restrict__ keep, int64_t n, int64_t *__restrict__ out,
-                                 int32_t *__restrict__ kept) {
+                                 int32_t *__restrict__ kept, const int32_t *__restrict__ status) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
-    const int64_t r = perm ? perm[keep[p]] : (int64_t)keep[p];
+    // failed selection (status set): keep the pool as it is (phys' = phys)
+    const int64_t r = (status && *status) ? p : perm ? perm[keep[p]] : (int64_t)keep[p];
     out[p] = phys[r];
     kept[r] = 1;
 }
@@ -1024,8 +1031,8 @@ extern "C" size_t temo_pool_update_ws_bytes(int64_t N) {
 }
 
 extern "C" int temo_pool_update(const int64_t *phys, const int64_t *perm, const int32_t *keep, int64_t N,
-                                int64_t n, int64_t *phys_out, void *ws, size_t ws_bytes,
-                                temo_stream_t stream) {
+                                int64_t n, int64_t *phys_out, const int32_t *status, void *ws,
+                                size_t ws_bytes, temo_stream_t stream) {
     if (N < 1 || n < 0 || n > N || !phys || !keep || !phys_out || phys_out == phys) return TEMO_EINVAL;
     if (!ws || ws_bytes < temo_pool_update_ws_bytes(N)) return TEMO_EWORKSPACE;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1035,7 +1042,7 @@ extern "C" int temo_pool_update(const int64_t *phys, const int64_t *perm, const 
     cub::DeviceScan::ExclusiveSum(nullptr, tb, fr, pos, (int)N);
     void *tmp = c.take<char>(tb);
     TEMO_CUDA(cudaMemsetAsync(kept, 0, sizeof(int32_t) * N, st));
-    if (n) k_pool_survivors<<<g1(n), NT, 0, st>>>(phys, perm, keep, n, phys_out, kept);
+    if (n) k_pool_survivors<<<g1(n), NT, 0, st>>>(phys, perm, keep, n, phys_out, kept, status);
     k_pool_free_flags<<<g1(N), NT, 0, st>>>(kept, N, fr);
     TEMO_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, fr, pos, (int)N, st));
     k_pool_free<<<g1(N), NT, 0, st>>>(phys, kept, pos, N, n, phys_out);

@@ -236,7 +236,8 @@ class _Stepper:
         """phys' = survivors' pool rows, then the freed rows (temo_pool_update)."""
         out = self.phys[1] if st.phys.data_ptr() == self.phys[0].data_ptr() else self.phys[0]
         rc = _lib.lib().temo_pool_update(_lib.ptr(st.phys), _lib.ptr(perm), _lib.ptr(keep), self.N, self.n,
-                                         _lib.ptr(out), _lib.ptr(self.pool_ws), self.pool_ws.numel(),
+                                         _lib.ptr(out), _lib.ptr(self.selector.status),
+                                         _lib.ptr(self.pool_ws), self.pool_ws.numel(),
                                          _lib.stream_handle(self.dev))
         _lib.check(rc, "pool_update")
         st.phys = out
@@ -267,6 +268,11 @@ class _Stepper:
             _lib.gather_rows(cur.F, keep, nxt.F[:n])
         st.cur, st.nxt = nxt, cur
         return st, time.perf_counter() - ts
+
+    def check(self):
+        """Raise the reference's exception if a selection failed (device status word)."""
+        if self.config.algorithm != "moead":
+            self.selector.check()
 
     def objectives(self, st: DeviceState):
         """F of the current population (device, logical order) -- no X materialisation."""
@@ -313,8 +319,11 @@ def run(config: RunConfig, sync_every_step: bool = True) -> RunRecord:
         F = stepper.objectives(st)
         ideal = F.min(dim=0).values.cpu().numpy().tolist() if sync_every_step else []
         total = time.perf_counter() - t0
+        if sync_every_step:
+            stepper.check()
         rows.append(GenRow(g, sel_s if config.time_selection_only else total, ideal))
     F = stepper.objectives(st)
     Fh = F.cpu().numpy()
+    stepper.check()
     mean = float(np.mean([r.time_s for r in rows])) if rows else math.nan
     return RunRecord(dataclasses.asdict(config), rows, mean, Fh)

@@ -201,6 +201,7 @@ class Nsga3Selector:
             self.Fs.copy_(Fs)
         if self.dist_rank is not None:
             r, l, nf = self.dist_rank(self.Fs, self.n, SELECT)
+            self.status.bitwise_or_(self.dist_rank.status)  # K0's NaN flag of the sharded rank
             self.rank.copy_(r)
             self.l.fill_(l)
             self.nfronts.fill_(nf)
@@ -236,9 +237,10 @@ def environmental_selection(X, F, R: DirectionSet, n: int, rng):
     N = Xd.shape[0]
     if Fd.shape[0] != N or N < n:
         raise ValueError("need matching X/F with at least n rows")
+    # the reference draws the shuffle first (nsga3.py:204) and raises inside rank_assign
+    perm = t.as_tensor(np.asarray(rng.permutation(N), dtype=np.int64)).to(Xd.device)
     if is_np and np.isnan(np.asarray(F, dtype=np.float64)).any():
         raise ValueError("objective matrix contains NaN rows")
-    perm = t.as_tensor(np.asarray(rng.permutation(N), dtype=np.int64)).to(Xd.device)
     sel = Nsga3Selector(N, Fd.shape[1], R, n, Xd.device)
     keep = sel.select(Fd, perm)
     Xn = t.empty((n, Xd.shape[1]), dtype=t.float64, device=Xd.device)

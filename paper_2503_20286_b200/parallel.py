@@ -180,6 +180,11 @@ class DistRank:
         self.backend = CudaShardBackend(N, m, lo, hi, dev)
         self.exchange = TorchDistExchange(self.bounds, mask_words(N), self.backend.dev, group)
 
+    @property
+    def status(self):
+        """Device status word of the shard (K0 flags NaN objectives here)."""
+        return self.backend.status
+
     def __call__(self, Fd, n: int, mode: int = SELECT):
         self.backend.build(Fd)
         rank, l, nf = run_sharded(self.backend, self.exchange, self.N, n, mode)

@@ -7,7 +7,10 @@ north star's 1e-5 relative tolerance.  LSMOP1 is new (the reference has no
 LSMOP): the standard definition of Cheng et al. 2017 in the PlatEMO
 formulation -- linear linkage x^s_i <- (1 + i/D) x^s_i - 10 x_1, chaotic
 subcomponent sizes (c <- 3.8 c (1 - c), nk = 5), Sphere g on every group and
-the linear front.
+the linear front.  As in PlatEMO, the requested dimension only sizes the
+subcomponents; the problem then has D = m - 1 + nk * sum(sublen) variables
+(``make_problem("lsmop1", 3, 1000)`` has D = 992) and the linkage divides by
+that D.
 """
 
 from __future__ import annotations
@@ -46,6 +49,26 @@ def lsmop_groups(m: int, d: int, nk: int = 5):
     return sublen, offset
 
 
+def lsmop_dimension(m: int, d_request: int, nk: int = 5):
+    """PlatEMO's D for a requested dimension: (D, sublen, offset); D = m - 1 + offset[m]."""
+    sublen, offset = lsmop_groups(m, d_request, nk)
+    return m - 1 + int(offset[m]), sublen, offset
+
+
+def lsmop_groups_for(m: int, D: int, nk: int = 5):
+    """(sublen, offset) of an LSMOP problem with D variables.
+
+    Every requested dimension that yields D yields the same groups (each floor
+    is monotone in the request), so D alone determines them."""
+    for d0 in range(D, D + nk * m + 2):
+        Dd, sublen, offset = lsmop_dimension(m, d0, nk)
+        if Dd == D:
+            return sublen, offset
+        if Dd > D:
+            break
+    raise ValueError(f"{D} is not an LSMOP dimension for m={m} (use make_problem with the requested D)")
+
+
 @dataclass(frozen=True)
 class ProblemSpec:
     """A DTLZ/LSMOP instance: name, decision dimension d, objective count m (problems.py:21-50)."""
@@ -64,6 +87,9 @@ class ProblemSpec:
         if self.d < self.m:
             raise ValueError("DTLZ needs d >= m")
         if self.name in LSMOP:
+            sub, _ = lsmop_groups_for(self.m, self.d)
+            if (sub < 1).any():
+                raise ValueError("LSMOP needs d large enough for every subcomponent")
             dl = np.zeros(self.d)
             du = np.concatenate([np.ones(self.m - 1), np.full(self.d - self.m + 1, 10.0)])
         else:
@@ -87,9 +113,7 @@ class ProblemSpec:
         if self.name in LSMOP:
             s.id = PROB_LSMOP1
             s.nk = 5
-            sub, off = lsmop_groups(self.m, self.d, 5)
-            if (sub < 1).any():
-                raise ValueError("LSMOP needs d large enough for every subcomponent")
+            sub, off = lsmop_groups_for(self.m, self.d, 5)
             for i in range(self.m):
                 s.sublen[i] = int(sub[i])
             for i in range(self.m + 1):
@@ -114,6 +138,13 @@ def make_problem(name: str, m: int = 3, d: int | None = None) -> ProblemSpec:
     name = name.lower()
     if d is None:
         d = default_dimension(name, m)
+    if name in LSMOP:  # d is PlatEMO's requested D; the instance has D = m - 1 + nk * sum(sublen)
+        if d < m:
+            raise ValueError("DTLZ needs d >= m")
+        sub, _ = lsmop_groups(m, d)
+        if (sub < 1).any():
+            raise ValueError("LSMOP needs d large enough for every subcomponent")
+        d = lsmop_dimension(m, d)[0]
     return ProblemSpec(name, d, m)
 
 

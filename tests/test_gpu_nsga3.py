@@ -224,3 +224,32 @@ def test_neighbors_golden(cuda):
     for c in cases(load_golden("neighbors")):
         got = neighbors(DirectionSet(c["W"], "simplex"), c["I"].shape[1]).I_nb
         assert np.array_equal(got, c["I"])
+
+
+def test_failed_selection_leaves_valid_keep_and_pool(cuda):
+    """A NaN objective row makes the selection fail (ValueError on check, nsga3.py:202 via
+    rank_assign); keep must still be a valid index set and the row pool must stay as it was,
+    so no downstream kernel reads garbage indices (k_keep_write / k_pool_survivors guards)."""
+    import torch
+
+    from paper_2503_20286_b200 import _lib
+    from paper_2503_20286_b200.directions import das_dennis
+    from paper_2503_20286_b200.nsga3 import Nsga3Selector
+
+    N, n, m = 200, 100, 3
+    F = np.random.default_rng(0).random((N, m))
+    F[17, 1] = np.nan
+    sel = Nsga3Selector(N, m, das_dennis(m, 12), n)
+    sel.keep.fill_(-12345)
+    keep = sel.select_shuffled(torch.from_numpy(F).cuda()).cpu().numpy()
+    assert np.array_equal(keep, np.arange(n))
+    with pytest.raises(ValueError):
+        sel.check()
+    phys = torch.arange(N, dtype=torch.int64, device=cuda).flip(0).contiguous()
+    out = torch.full((N,), -1, dtype=torch.int64, device=cuda)
+    ws = torch.empty(max(int(_lib.lib().temo_pool_update_ws_bytes(N)), 256), dtype=torch.uint8, device=cuda)
+    perm = torch.arange(N, dtype=torch.int64, device=cuda)
+    rc = _lib.lib().temo_pool_update(_lib.ptr(phys), _lib.ptr(perm), _lib.ptr(sel.keep), N, n, _lib.ptr(out),
+                                     _lib.ptr(sel.status), _lib.ptr(ws), ws.numel(), _lib.stream_handle(cuda))
+    assert rc == 0
+    assert torch.equal(out, phys)

@@ -107,6 +107,7 @@ def test_lsmop1_vs_self_oracle(cuda, m, d):
     from paper_2503_20286_b200.problems import evaluate, make_problem
 
     spec = make_problem("lsmop1", m=m, d=d)
+    d = spec.d  # PlatEMO's D for the requested dimension
     rng = np.random.default_rng(d)
     X = spec.lower + rng.random((200, d)) * (spec.upper - spec.lower)
     assert np.allclose(evaluate(spec, X), oprob.evaluate_lsmop1(X, m), rtol=1e-12, atol=0)
@@ -122,6 +123,7 @@ def test_fused_offspring_matches_oracle(cuda, name, m, d, n):
 
     spec = make_problem(name, m=m, d=d)
     cfg = RunConfig(algorithm="nsga3", problem=name, objectives=m, dim=d, pop_size=n)
+    d = spec.d
     st_ = _Stepper(cfg, spec, das_dennis(m, 4), n)
     g_dev, g_ref = philox_gen(3), philox_gen(3)
     state = st_.init(g_dev)
@@ -183,6 +185,7 @@ def test_offspring_two_phase_equals_fused(cuda, name, m, d, h, pre):
     from paper_2503_20286_b200.variation import VariationParams
 
     spec = make_problem(name, m=m, d=d)
+    d = spec.d
     dev = torch.device("cuda", 0)
     var = VariationParams(lower=spec.lower, upper=spec.upper).struct(d, dev)
     prob = spec.struct()

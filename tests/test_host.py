@@ -69,10 +69,15 @@ def test_lsmop_descriptor_matches_self_oracle():
         b = oprob.lsmop_groups(m, d)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
         spec = make_problem("lsmop1", m=m, d=d)
-        lo, hi = oprob.lsmop_bounds(m, d)
+        # PlatEMO: the request sizes the groups, then D = m - 1 + nk * sum(sublen)
+        assert spec.d == m - 1 + a[1][m] == oprob.lsmop_dimension(m, d)
+        lo, hi = oprob.lsmop_bounds(m, spec.d)
         assert np.array_equal(spec.lower, lo) and np.array_equal(spec.upper, hi)
         s = spec.struct()
-        assert s.id == 101 and s.nk == 5 and s.sublen[0] == a[0][0]
+        assert s.id == 101 and s.nk == 5 and s.sublen[0] == a[0][0] and s.offset[m] == a[1][m]
+        b2 = oprob.lsmop_groups_for(m, spec.d)
+        assert np.array_equal(a[0], b2[0]) and np.array_equal(a[1], b2[1])
+    assert make_problem("lsmop1", m=3, d=1000).d == 992
 
 
 def test_run_config_validation():
@@ -85,7 +90,7 @@ def test_run_config_validation():
     spec, R, n = _resolve(RunConfig(algorithm="moead", problem="dtlz2", pop_size=100))
     assert n == R.count == 91
     spec, R, n = _resolve(RunConfig(algorithm="nsga3", problem="lsmop1", dim=1000, pop_size=200_000))
-    assert R.count == 199_396 and n == 200_000 and spec.d == 1000
+    assert R.count == 199_396 and n == 200_000 and spec.d == 992  # PlatEMO D for the request 1000
 
 
 def test_moead_default_neighborhood():
