@@ -68,6 +68,18 @@ int temo_rank(const double *F, int64_t N, int m, int64_t n, int mode, int32_t *r
               int32_t *l_out, int32_t *nfronts, int32_t *status, void *ws, size_t ws_bytes,
               temo_stream_t stream);
 
+/* Path selection (diagnostics / A-B comparisons): m = 2 and 3 use the staircase
+ * sort (lex-prefix merge-sort tree, ndsort_stair.cuh); temo_rank_force_bitmap(1)
+ * (or env TEMO_RANK_BITMAP=1) sends them through the O(N^2) bitmap path like
+ * m >= 4.  Both give identical ranks; set it before sizing the workspace. */
+void temo_rank_force_bitmap(int on);
+/* Diagnostics: per-front phase timestamps (%globaltimer, ns) of the staircase peel's
+ * block 0, 8 per front: front start, phase A done, barrier 1 passed, high levels done,
+ * high levels done, tile levels done, front written, barrier 2 passed; `on` = 1 + the
+ * profiled block (0: off). */
+void temo_stair_prof_enable(int on);
+int temo_stair_prof_read(uint64_t *host, int64_t count);
+
 /* Dominance bitmap only (ndsort.dominance_matrix, ndsort.py:25-44):
  * D_out is N x ceil(N/32) uint32 words, bit (j%32) of word [i][j/32] set iff
  * row i dominates row j.  For parity tests at small N. */

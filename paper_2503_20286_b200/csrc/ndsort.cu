@@ -1341,13 +1341,24 @@ static int peel_grid(int NB, size_t smem) {
 
 }  // namespace temo
 
+#include "ndsort_stair.cuh"
+
 using namespace temo;
 
-extern "C" size_t temo_rank_ws_bytes(int64_t N, int m) {
-    if (N < 1 || m < 1 || m > MAX_M) return 0;
+static size_t bitmap_ws_bytes(int64_t N, int m) {
     RankPlan p;
     plan_rank(p, nullptr, N, m);
     return p.total;
+}
+
+extern "C" size_t temo_rank_ws_bytes(int64_t N, int m) {
+    if (N < 1 || m < 1 || m > MAX_M) return 0;
+    if (use_stair(m)) {
+        StairPlan s;
+        plan_stair(s, nullptr, N, m);
+        return s.total;
+    }
+    return bitmap_ws_bytes(N, m);
 }
 
 extern "C" int temo_rank(const double *F, int64_t N, int m, int64_t n, int mode, int32_t *rank,
@@ -1357,6 +1368,13 @@ extern "C" int temo_rank(const double *F, int64_t N, int m, int64_t n, int mode,
     if (n < 1 || n > N) return TEMO_EINVAL;
     if (mode != TEMO_RANK_SORT && mode != TEMO_RANK_SELECT) return TEMO_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
+    if (use_stair(m)) {
+        StairPlan s;
+        plan_stair(s, nullptr, N, m);
+        if (ws_bytes < s.total || !ws) return TEMO_EWORKSPACE;
+        plan_stair(s, ws, N, m);
+        return stair_rank(s, F, n, mode, rank, l_out, nfronts, status, st);
+    }
     RankPlan p;
     plan_rank(p, nullptr, N, m);
     if (ws_bytes < p.total || !ws) return TEMO_EWORKSPACE;
@@ -1391,7 +1409,8 @@ extern "C" int temo_rank(const double *F, int64_t N, int m, int64_t n, int mode,
 }
 
 extern "C" size_t temo_dominance_ws_bytes(int64_t N, int m) {
-    return temo_rank_ws_bytes(N, m) + (size_t)N * 4 + 256;
+    if (N < 1 || m < 1 || m > MAX_M) return 0;
+    return bitmap_ws_bytes(N, m) + (size_t)N * 4 + 256;
 }
 
 extern "C" int temo_dominance(const double *F, int64_t N, int m, uint32_t *D_out, int32_t *status,

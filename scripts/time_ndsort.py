@@ -13,8 +13,12 @@ from paper_2503_20286_b200.ndsort import SELECT, SORT, rank_device  # noqa: E402
 
 
 def main():
-    sizes = [int(a) for a in sys.argv[1:]] or [20000, 100000, 400000]
-    for m in (3,):
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    sizes = [int(a) for a in args] or [20000, 100000, 400000]
+    ms_list = [int(x) for x in os.environ.get("MS", "3").split(",")]
+    if "--bitmap" in sys.argv:
+        _lib.lib().temo_rank_force_bitmap(1)
+    for m in ms_list:
         for N in sizes:
             F = torch.from_numpy(np.random.default_rng(0).random((N, m))).cuda()
             for mode in (SORT, SELECT):

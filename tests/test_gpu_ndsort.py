@@ -174,3 +174,55 @@ def test_large_property_equivariance(cuda):
         dom = np.all(F <= F[j], axis=1) & np.any(F < F[j], axis=1)
         want = 0 if not dom.any() else int(r1[dom].max()) + 1
         assert r1[j] == want
+
+
+def _rank_both(Fd, n, mode):
+    """(staircase, bitmap) results of temo_rank for the same input."""
+    from paper_2503_20286_b200 import _lib
+    from paper_2503_20286_b200.ndsort import rank_device
+
+    outs = []
+    for force in (0, 1):
+        _lib.lib().temo_rank_force_bitmap(force)
+        try:
+            r, l, nf = rank_device(Fd, n, mode)
+            outs.append((r.cpu().numpy(), int(l.item()), int(nf.item())))
+        finally:
+            _lib.lib().temo_rank_force_bitmap(0)
+    return outs
+
+
+@pytest.mark.parametrize("N,m,kind", [(1, 3, "u"), (2, 2, "u"), (3, 3, "i"), (2047, 3, "u"), (2048, 3, "i"),
+                                      (2049, 2, "u"), (4097, 3, "dup"), (30000, 3, "i"), (65537, 3, "u"),
+                                      (70000, 2, "i"), (131072, 3, "dup"), (400_000, 3, "lsmop"),
+                                      (300_001, 2, "u"), (500_000, 3, "u")])
+def test_staircase_equals_bitmap(cuda, N, m, kind):
+    """The m <= 3 staircase sort (ndsort_stair.cuh) against the O(N^2) bitmap path (K1 + peel):
+    identical ranks, l and front counts in SORT and SELECT mode, across tile (2048) and level
+    boundaries, integer ties, exact duplicate rows (-0.0 / +0.0) and the LSMOP1 distribution."""
+    import torch
+
+    from paper_2503_20286_b200.ndsort import SELECT, SORT
+
+    rng = np.random.default_rng(N * 7 + m)
+    if kind == "u":
+        F = rng.random((N, m))
+    elif kind == "i":
+        F = rng.integers(0, 40, size=(N, m)).astype(float)
+    elif kind == "dup":
+        base = rng.random((max(N // 5, 1), m))
+        F = base[rng.integers(0, len(base), N)]
+        F[rng.random(N) < 0.05, 0] = -0.0
+        F[rng.random(N) < 0.05, 1] = 0.0
+    else:  # LSMOP1-like objectives: (1 + g) * linear front
+        x = rng.random((N, 2))
+        g = rng.random(N)[:, None] * 50
+        F = (1 + g) * np.stack([x[:, 0] * x[:, 1], x[:, 0] * (1 - x[:, 1]), 1 - x[:, 0]], 1)
+    Fd = torch.from_numpy(F).cuda()
+    for mode in (SORT, SELECT):
+        if mode == SORT and N > 131072:
+            continue  # the bitmap SORT at 400k+ is slow; SELECT covers the headline
+        n = max(N // 2, 1)
+        (ra, la, fa), (rb, lb, fb) = _rank_both(Fd, n, mode)
+        assert la == lb and fa == fb, (mode, la, lb, fa, fb)
+        assert np.array_equal(ra, rb), mode
