@@ -172,6 +172,25 @@ typedef struct temo_philox_state {
     int32_t reserved;
 } temo_philox_state;
 
+/* Full host state of NumPy's Philox bit generator (Philox.state: counter, key,
+ * buffer, buffer_pos, has_uint32, uinteger). */
+typedef struct temo_philox_host {
+    uint64_t counter[4];
+    uint64_t key[2];
+    uint64_t buffer[4];
+    int32_t buffer_pos;
+    int32_t has_uint32;
+    uint32_t uinteger;
+    uint32_t reserved;
+} temo_philox_host;
+
+/* Host (CPU) replica of Generator.permutation(n) (variation.py:52, nsga3.py:204):
+ * arange(n) Fisher-Yates-shuffled with NumPy's random_interval draws, bit for bit;
+ * `st` is advanced exactly as NumPy advances the Generator.  Native host code,
+ * no GPU involved (the reference's sequential shuffle is the host-side bound of
+ * the generation loop). */
+int temo_host_permutation(temo_philox_host *st, int64_t n, int64_t *out);
+
 #define TEMO_PROB_DTLZ1 1 /* ... TEMO_PROB_DTLZ1 + 6 = DTLZ7 (problems.py:105-136) */
 #define TEMO_PROB_LSMOP1 101 /* LSMOP1, Cheng et al. 2017 (no reference; self-oracle) */
 

@@ -35,6 +35,7 @@ SIGNATURES = {
     "temo_rank_ws_bytes": (_SZ, [_I64, _I32]),
     "temo_rank": (_I32, [_P, _I64, _I32, _I64, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
     "temo_rank_force_bitmap": (None, [_I32]),
+    "temo_host_permutation": (_I32, [_P, _I64, _P]),
     "temo_stair_prof_enable": (None, [_I32]),
     "temo_stair_prof_read": (_I32, [_P, _I64]),
     "temo_dominance_ws_bytes": (_SZ, [_I64, _I32]),

@@ -31,6 +31,7 @@ from .directions import DirectionSet, das_dennis, largest_h_for, neighbors
 from .nsga3 import Nsga3Selector
 from .problems import ProblemSpec, make_problem
 from .rng import DeviceDraws, RngStream
+from .rng import permutation as rng_permutation
 from .variation import VariationParams
 
 ALGORITHMS = ("nsga3", "moead", "hype")
@@ -202,7 +203,7 @@ class _Stepper:
 
     # -- offspring of NSGA-III / HypE (harness.py:201-204, 218-222) into rows [n, N)
     def _offspring(self, st: DeviceState, gen):
-        i1, i2 = (lambda p, h: (p[:h], p[h: 2 * h]))(gen.permutation(self.n), self.h)
+        i1, i2 = (lambda p, h: (p[:h], p[h: 2 * h]))(rng_permutation(gen, self.n), self.h)
         self.ring.upload(np.concatenate([i1, i2]).astype(np.int64), self.i12)
         draws = DeviceDraws(gen)
         hd = self.h * self.spec.d
@@ -258,7 +259,7 @@ class _Stepper:
         cur, nxt = st.cur, st.nxt
         n = self.n
         if alg == "nsga3":
-            self.ring.upload(np.asarray(gen.permutation(self.N), dtype=np.int64), self.perm)
+            self.ring.upload(rng_permutation(gen, self.N), self.perm)
             keep = self.selector.select(cur.F, self.perm)
             self._pool_update(st, self.perm, keep)  # survivors' X rows stay where they are
             _lib.gather_rows(self.selector.Fs, keep, nxt.F[:n])

@@ -19,6 +19,7 @@ import numpy as np
 from . import _lib
 from .directions import DirectionSet
 from .ndsort import SELECT, rank_device
+from .rng import permutation as rng_permutation
 
 BIG = np.finfo(np.float64).max  # tensorops.py:18
 
@@ -238,7 +239,7 @@ def environmental_selection(X, F, R: DirectionSet, n: int, rng):
     if Fd.shape[0] != N or N < n:
         raise ValueError("need matching X/F with at least n rows")
     # the reference draws the shuffle first (nsga3.py:204) and raises inside rank_assign
-    perm = t.as_tensor(np.asarray(rng.permutation(N), dtype=np.int64)).to(Xd.device)
+    perm = t.as_tensor(rng_permutation(rng, N)).to(Xd.device)
     if is_np and np.isnan(np.asarray(F, dtype=np.float64)).any():
         raise ValueError("objective matrix contains NaN rows")
     sel = Nsga3Selector(N, Fd.shape[1], R, n, Xd.device)

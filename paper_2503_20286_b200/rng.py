@@ -46,6 +46,46 @@ class PhiloxState(ctypes.Structure):
                 ("reserved", ctypes.c_int32)]
 
 
+class PhiloxHostState(ctypes.Structure):
+    """Mirror of ``temo_philox_host`` (include/temo_b200.h): the full NumPy Philox state."""
+
+    _fields_ = [("counter", ctypes.c_uint64 * 4), ("key", ctypes.c_uint64 * 2),
+                ("buffer", ctypes.c_uint64 * 4), ("buffer_pos", ctypes.c_int32),
+                ("has_uint32", ctypes.c_int32), ("uinteger", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
+
+
+def permutation(rng, n: int) -> np.ndarray:
+    """``rng.permutation(n)`` (int64), drawn by the native replica for Philox Generators.
+
+    Bit-identical to NumPy (``temo_host_permutation``) and the Generator ends in the
+    same state; any other RNG object is called directly (duck-typed test RNGs)."""
+    n = int(n)
+    if not is_philox(rng) or n < 2:
+        return np.asarray(rng.permutation(n), dtype=np.int64)
+    from . import _lib
+
+    st = rng.bit_generator.state
+    s = PhiloxHostState()
+    for i in range(4):
+        s.counter[i] = int(st["state"]["counter"][i])
+        s.buffer[i] = int(st["buffer"][i])
+    s.key[0], s.key[1] = int(st["state"]["key"][0]), int(st["state"]["key"][1])
+    s.buffer_pos = int(st["buffer_pos"])
+    s.has_uint32 = int(st["has_uint32"])
+    s.uinteger = int(st["uinteger"])
+    out = np.empty(n, dtype=np.int64)
+    rc = _lib.lib().temo_host_permutation(ctypes.byref(s), n, out.ctypes.data_as(ctypes.c_void_p))
+    _lib.check(rc, "permutation")
+    st["state"]["counter"] = np.array(list(s.counter), dtype=np.uint64)
+    st["buffer"] = np.array(list(s.buffer), dtype=np.uint64)
+    st["buffer_pos"] = int(s.buffer_pos)
+    st["has_uint32"] = int(s.has_uint32)
+    st["uinteger"] = int(s.uinteger)
+    rng.bit_generator.state = st
+    return out
+
+
 def is_philox(rng) -> bool:
     return isinstance(rng, np.random.Generator) and isinstance(rng.bit_generator, np.random.Philox)
 

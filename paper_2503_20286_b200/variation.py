@@ -17,6 +17,7 @@ import numpy as np
 
 from . import _lib
 from .rng import DeviceDraws, is_philox
+from .rng import permutation as rng_permutation
 
 
 class VariationStruct(ctypes.Structure):
@@ -76,7 +77,7 @@ def pair_parents(rng, n: int):
     """Split a random permutation into two mating halves (variation.py:48-54)."""
     if n < 2:
         raise ValueError("need at least two individuals to pair")
-    perm = rng.permutation(n)
+    perm = rng_permutation(rng, n)
     half = n // 2
     return perm[:half], perm[half: 2 * half]
 

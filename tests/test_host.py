@@ -109,3 +109,28 @@ def test_variation_params_validation():
     with pytest.raises(ValueError):
         VariationParams(lower=np.ones(3), upper=np.zeros(3))
     assert VariationParams(lower=np.zeros(4), upper=np.ones(4)).mutation_prob(4) == 0.25
+
+
+def test_host_permutation_bit_exact_with_numpy():
+    """temo_host_permutation (native Fisher-Yates + random_interval over Philox next_uint32)
+    equals Generator.permutation and leaves the identical Generator state, for every buffer
+    position / pending-half-word state and across mask classes (variation.py:52, nsga3.py:204)."""
+    from paper_2503_20286_b200 import rng as R
+
+    def same(sa, sb):
+        return (all(np.array_equal(sa["state"][k], sb["state"][k]) for k in ("counter", "key"))
+                and np.array_equal(sa["buffer"], sb["buffer"])
+                and all(sa[k] == sb[k] for k in ("buffer_pos", "has_uint32", "uinteger")))
+
+    for seed in range(4):
+        for pre in range(5):
+            for n in (2, 3, 17, 64, 65, 1025, 4097, 65537, 200_003):
+                a = np.random.Generator(np.random.Philox(seed))
+                b = np.random.Generator(np.random.Philox(seed))
+                a.random(pre)
+                b.random(pre)
+                a.integers(0, 7, pre)  # leaves a pending 32-bit half for odd counts
+                b.integers(0, 7, pre)
+                assert np.array_equal(a.permutation(n), R.permutation(b, n)), (seed, pre, n)
+                assert same(a.bit_generator.state, b.bit_generator.state), (seed, pre, n)
+                assert np.array_equal(a.random(3), b.random(3))
