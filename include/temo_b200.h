@@ -331,15 +331,21 @@ int temo_hype_select(const double *F, int64_t N, int m, int64_t n, int64_t s, co
  * 1 <= T <= min(r, 64), m <= 16. */
 int temo_neighbors(const double *W, int64_t r, int m, int T, int32_t *out, temo_stream_t stream);
 
-/* Diagnostic microbenchmark: issue rate (compares/s) of a register-only ISETP + VOTE mix.
- * Not a roofline denominator (bench.py derives K1's ceiling from the SM issue rate). */
-double temo_probe_compare_rate(int blocks, int iters, temo_stream_t stream);
+/* Measured ceilings for bench.py's roofline_compute denominators (probe.cu): the inner-loop
+ * instruction mix of a compute-bound kernel on register operands only.
+ *   temo_probe_philox_rate : Philox4x64-10 blocks/s (k_offspring_rand's core)
+ *   temo_probe_packed_rate : packed dominance pair tests/s (k_dom_rows8's step, m = 3)
+ *   temo_probe_dsub_rate   : FP64 add/sub operations/s (k_hv_dom's sample test)
+ * scratch: 8 bytes of device memory (written only to keep the work live). */
+double temo_probe_philox_rate(int blocks, int iters, uint64_t *scratch, temo_stream_t stream);
+double temo_probe_packed_rate(int blocks, int iters, uint64_t *scratch, temo_stream_t stream);
+double temo_probe_dsub_rate(int blocks, int iters, uint64_t *scratch, temo_stream_t stream);
 
 /* ------------------------------------------------------------ stage timing
  * CUDA-event timing of each kernel stage on its own stream (off by default).
  * temo_timing_read syncs the recorded events, fills ms_out/calls_out
  * (TEMO_STAGE_COUNT entries each) and optionally resets the accumulators. */
-#define TEMO_STAGE_COUNT 14
+#define TEMO_STAGE_COUNT 15
 void temo_timing_enable(int on);
 const char *temo_timing_name(int stage);
 int temo_timing_read(double *ms_out, int64_t *calls_out, int reset);

@@ -80,12 +80,14 @@ SIGNATURES = {
     "temo_hype_select_ws_bytes": (_SZ, [_I64, _I32, _I64]),
     "temo_hype_select": (_I32, [_P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P,
                                 _SZ, _P]),
-    "temo_probe_compare_rate": (_D, [_I32, _I32, _P]),
+    "temo_probe_philox_rate": (_D, [_I32, _I32, _P, _P]),
+    "temo_probe_packed_rate": (_D, [_I32, _I32, _P, _P]),
+    "temo_probe_dsub_rate": (_D, [_I32, _I32, _P, _P]),
     "temo_timing_enable": (None, [_I32]),
     "temo_timing_name": (ctypes.c_char_p, [_I32]),
     "temo_timing_read": (_I32, [_P, _P, _I32]),
 }
-STAGE_COUNT = 14
+STAGE_COUNT = 15
 
 TEMO_OK, TEMO_EINVAL, TEMO_ENAN, TEMO_ERUNTIME, TEMO_EWORKSPACE, TEMO_ECUDA = range(6)
 ST_NAN, ST_PEEL, ST_FILL, ST_DEMOTE, ST_COUNT, ST_KRANGE = 1, 2, 4, 8, 16, 32
@@ -110,7 +112,10 @@ def lib():
     with _lock:
         if _handle is None:
             path = _build.LIB
-            if not _build.up_to_date() and os.environ.get("TEMO_NO_BUILD") != "1":
+            override = os.environ.get("TEMO_LIB")  # A/B experiments: an alternative build of the library
+            if override:
+                path = Path(override).resolve()
+            elif not _build.up_to_date() and os.environ.get("TEMO_NO_BUILD") != "1":
                 _build.build()
             if not path.exists():
                 raise TemoError(f"CUDA library missing: {path} (run __graft_entry__.build())")

@@ -55,7 +55,8 @@ int num_sms();
 // stage ids for temo_timing_* (names in capi.cu)
 enum Stage {
     S_RANK_PREP = 0, S_DOM_BITS, S_PEEL, S_NORMALIZE, S_ASSOCIATE, S_NICHE, S_OFFSPRING,
-    S_EVALUATE, S_HV_COUNT, S_HV_CONTRIB, S_HYPE_SELECT, S_MOEAD, S_GATHER, S_MISC
+    S_EVALUATE, S_HV_COUNT, S_HV_CONTRIB, S_HYPE_SELECT, S_MOEAD, S_GATHER, S_MISC,
+    S_OFFSPRING_APPLY  // the apply kernel of the two-phase offspring step (S_OFFSPRING: its randomness kernel)
 };
 void stage_begin(int stage, cudaStream_t st);
 void stage_end(int stage, cudaStream_t st);

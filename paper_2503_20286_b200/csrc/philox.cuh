@@ -18,6 +18,7 @@ struct Philox {
     uint64_t key[2];
     uint64_t buf[4];
     int32_t pos;
+    uint64_t rk[20];  // round keys (k0, k1) of rounds 0..9: kernel-parameter (constant bank) operands
 };
 
 __host__ __device__ inline Philox philox_from(const temo_philox_state &s) {
@@ -26,6 +27,15 @@ __host__ __device__ inline Philox philox_from(const temo_philox_state &s) {
     p.key[0] = s.key[0];
     p.key[1] = s.key[1];
     p.pos = s.buffer_pos;
+    uint64_t k0 = s.key[0], k1 = s.key[1];
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B97F4A7C15ull;
+            k1 += 0xBB67AE8584CAA73Bull;
+        }
+        p.rk[2 * r] = k0;
+        p.rk[2 * r + 1] = k1;
+    }
     return p;
 }
 
@@ -88,6 +98,34 @@ __device__ __forceinline__ void philox_blocks(const uint64_t ctr[NB][4], const u
     }
 }
 
+// NB independent blocks with precomputed round keys (no per-round key additions)
+template <int NB>
+__device__ __forceinline__ void philox_blocks_rk(const uint64_t ctr[NB][4], const uint64_t *rk,
+                                                 uint64_t out[NB][4]) {
+    uint64_t c0[NB], c1[NB], c2[NB], c3[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        c0[b] = ctr[b][0]; c1[b] = ctr[b][1]; c2[b] = ctr[b][2]; c3[b] = ctr[b][3];
+    }
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const uint64_t lo0 = 0xD2E7470EE14C6C93ull * c0[b], hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c0[b]);
+            const uint64_t lo1 = 0xCA5A826395121157ull * c2[b], hi1 = __umul64hi(0xCA5A826395121157ull, c2[b]);
+            const uint64_t n0 = hi1 ^ c1[b] ^ rk[2 * r], n2 = hi0 ^ c3[b] ^ rk[2 * r + 1];
+            c0[b] = n0;
+            c1[b] = lo1;
+            c2[b] = n2;
+            c3[b] = lo0;
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        out[b][0] = c0[b]; out[b][1] = c1[b]; out[b][2] = c2[b]; out[b][3] = c3[b];
+    }
+}
+
 // counter + add (256-bit, little-endian words)
 __device__ __forceinline__ void ctr_add(const uint64_t in[4], uint64_t add, uint64_t out[4]) {
     out[0] = in[0] + add;
@@ -109,9 +147,10 @@ struct PhiloxCursor {
         if (e < avail) return p.buf[p.pos + e];
         const uint64_t e2 = e - avail, b = e2 >> 2;
         if (b != blk) {
-            uint64_t c[4];
-            ctr_add(p.ctr, b + 1, c);
-            philox_block(c, p.key, v);
+            uint64_t c[1][4], o[1][4];
+            ctr_add(p.ctr, b + 1, c[0]);
+            philox_blocks_rk<1>(c, p.rk, o);
+            for (int k = 0; k < 4; ++k) v[k] = o[0][k];
             blk = b;
         }
         return v[e2 & 3];

@@ -1,50 +1,151 @@
-// Diagnostic microbenchmark: the first K1 design's inner-loop instruction mix
-// (two chained unsigned ISETP + one warp VOTE per (warp, row)) on register
-// operands only.  Kept as a probe of the compare/vote issue rate; the packed K1
-// beats it, so it is not used as a roofline denominator (bench.py uses the SM
-// issue rate).
+// Measured ceilings for the roofline denominators of the two compute-bound kernels
+// (bench.py `roofline_compute`).  Neither is on the data path; each runs the
+// kernel's inner-loop instruction mix on register operands only, so its rate is
+// the issue/pipe ceiling of that mix on this GPU and clock.
+//
+//   k_probe_philox : Philox4x64-10 blocks (NumPy's stream, philox.cuh), 4 blocks in
+//                    lockstep per thread -- the core of k_offspring_rand (5 blocks per
+//                    gene quad).  Rate = blocks/s.
+//   k_probe_packed : the packed dominance step of K1 (ndsort.cu k_dom_rows8, m = 3):
+//                    per column pair 2 IMAD subtractions, one LOP3, one LEA/shift-add.
+//                    Rate = pair tests/s (2 per step).
+//   k_probe_dsub   : FP64 subtract + add chains (HypE's sample-dominance test).  Rate =
+//                    FP64 add/sub operations/s.
+// The caller passes an 8-byte device scratch word (the library allocates nothing).
 #include "common.cuh"
+#include "philox.cuh"
 
 namespace temo {
 
-__global__ void __launch_bounds__(256) k_probe_compare(int iters, uint32_t seed, uint32_t *out) {
-    uint32_t a = seed ^ (threadIdx.x * 2654435761u), b = a * 7u + 3u;
-    uint32_t r1 = a & 0xFFFFF, r2 = b & 0xFFFFF;
-    uint32_t acc = 0;
+__global__ void __launch_bounds__(256) k_probe_philox(Philox ph, int iters, uint64_t *out) {
+    uint64_t c[4][4];
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) ctr_add(ph.ctr, 4 * t + b, c[b]);
+    uint64_t acc = 0;
     for (int it = 0; it < iters; ++it) {
-#pragma unroll 16
-        for (int k = 0; k < 16; ++k) {
-            // operands vary per step but stay in registers (like LDS broadcasts of i)
-            const uint32_t x = (r1 + k * 977u) & 0xFFFFF, y = (r2 + k * 1931u) & 0xFFFFF;
-            const bool P = (x <= r1) & (y <= r2);
-            acc ^= __ballot_sync(~0u, P);
+        uint64_t o[4][4];
+        philox_blocks_rk<4>(c, ph.rk, o);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            acc ^= o[b][0] ^ o[b][1] ^ o[b][2] ^ o[b][3];
+            c[b][0] += 0x100000000ull;  // next counters (stays in the low word's upper half)
         }
-        r1 += acc & 1;
-        r2 ^= acc >> 31;
     }
-    if (acc == 0x12345678u) out[0] = acc;  // keep the work live
+    if (acc == 0x123456789ull) out[0] = acc;  // keep the work live
+}
+
+__global__ void __launch_bounds__(128) k_probe_packed(int iters, uint32_t seed, uint64_t *out) {
+    // 8 rows per lane (k_dom_rows8), column-pair words broadcast: per step and row
+    // g = ((Q1 | G) - p1 * 0x10001) & ((Q2 | G) - p2 * 0x10001) & 0x80008000; acc = (acc >> 1) + g
+    uint32_t p1[8], p2[8], acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        p1[r] = (seed + threadIdx.x * 31u + r * 7u) & 0x7FF;
+        p2[r] = (seed * 3u + threadIdx.x * 17u + r * 5u) & 0x7FF;
+        acc[r] = 0;
+    }
+    uint32_t q1 = seed * 2654435761u, q2 = seed * 40503u;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const uint32_t a = (q1 + s * 0x00010001u) | 0x80008000u, b = (q2 + s * 0x00030003u) | 0x80008000u;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint32_t g = (a - p1[r] * 0x10001u) & (b - p2[r] * 0x10001u) & 0x80008000u;
+                acc[r] = (acc[r] >> 1) + g;
+            }
+        }
+        q1 += acc[0];
+        q2 ^= acc[7];
+    }
+    uint32_t x = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) x ^= acc[r];
+    if (x == 0x12345678u) out[0] = x;
+}
+
+// HypE's dominance test (hype.cu k_hv_dom): per (point, sample, objective) one FP64
+// subtraction whose sign bits are OR-ed; 8 independent chains per thread.
+__global__ void __launch_bounds__(256) k_probe_dsub(int iters, double seed, uint64_t *out) {
+    double f[8], acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        f[r] = seed + 0.125 * r + 1e-3 * threadIdx.x;
+        acc[r] = 0.0;
+    }
+    double smp = seed * 0.5;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const double x = smp + 0.0625 * s;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) acc[r] = acc[r] + (x - f[r]);
+        }
+        smp = smp + acc[0] * 1e-300;
+    }
+    double x = 0.0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) x += acc[r];
+    if (x == 1234.5) out[0] = 1;
 }
 
 }  // namespace temo
 
-// Returns compares per second (2 compares per lane per step) measured with CUDA events.
-extern "C" double temo_probe_compare_rate(int blocks, int iters, temo_stream_t stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    uint32_t *dummy = nullptr;
-    if (cudaMalloc(&dummy, 4) != cudaSuccess) return -1.0;
+namespace {
+double time_launches(void (*launch)(cudaStream_t, int), int iters, cudaStream_t st) {
     cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    temo::k_probe_compare<<<blocks, 256, 0, st>>>(iters / 4, 1u, dummy);  // warm-up
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return -1.0;
+    launch(st, iters / 4 > 0 ? iters / 4 : 1);  // warm-up
     cudaEventRecord(a, st);
-    temo::k_probe_compare<<<blocks, 256, 0, st>>>(iters, 1u, dummy);
+    launch(st, iters);
     cudaEventRecord(b, st);
     cudaEventSynchronize(b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    cudaFree(dummy);
-    const double lanes = (double)blocks * 256.0;
-    return lanes * (double)iters * 16.0 * 2.0 / (ms * 1e-3);
+    return cudaGetLastError() == cudaSuccess ? ms * 1e-3 : -1.0;
+}
+
+int g_blocks;
+uint64_t *g_scratch;
+void launch_philox(cudaStream_t st, int iters) {
+    temo_philox_state z = {};
+    z.buffer_pos = 4;
+    temo::k_probe_philox<<<g_blocks, 256, 0, st>>>(temo::philox_from(z), iters, g_scratch);
+}
+void launch_packed(cudaStream_t st, int iters) {
+    temo::k_probe_packed<<<g_blocks, 128, 0, st>>>(iters, 1u, g_scratch);
+}
+void launch_dsub(cudaStream_t st, int iters) {
+    temo::k_probe_dsub<<<g_blocks, 256, 0, st>>>(iters, 1.0, g_scratch);
+}
+}  // namespace
+
+// Philox4x64-10 blocks per second (4 blocks per thread per iteration), CUDA events.
+extern "C" double temo_probe_philox_rate(int blocks, int iters, uint64_t *scratch, temo_stream_t stream) {
+    if (blocks < 1 || iters < 1 || !scratch) return -1.0;
+    g_blocks = blocks;
+    g_scratch = scratch;
+    const double s = time_launches(launch_philox, iters, (cudaStream_t)stream);
+    return s > 0 ? (double)blocks * 256.0 * 4.0 * iters / s : -1.0;
+}
+
+// Packed dominance pair tests per second (k_dom_rows8 inner step, m = 3), CUDA events.
+extern "C" double temo_probe_packed_rate(int blocks, int iters, uint64_t *scratch, temo_stream_t stream) {
+    if (blocks < 1 || iters < 1 || !scratch) return -1.0;
+    g_blocks = blocks;
+    g_scratch = scratch;
+    const double s = time_launches(launch_packed, iters, (cudaStream_t)stream);
+    return s > 0 ? (double)blocks * 128.0 * 8.0 * 16.0 * 2.0 * iters / s : -1.0;
+}
+
+// FP64 add/subtract operations per second (2 per step and chain: x - f, acc + .), CUDA events.
+extern "C" double temo_probe_dsub_rate(int blocks, int iters, uint64_t *scratch, temo_stream_t stream) {
+    if (blocks < 1 || iters < 1 || !scratch) return -1.0;
+    g_blocks = blocks;
+    g_scratch = scratch;
+    const double s = time_launches(launch_dsub, iters, (cudaStream_t)stream);
+    return s > 0 ? (double)blocks * 256.0 * 8.0 * 16.0 * 2.0 * iters / s : -1.0;
 }

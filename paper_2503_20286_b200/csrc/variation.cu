@@ -29,13 +29,22 @@ __device__ __forceinline__ double clipv(double x, double lo, double hi) {
     return y > hi ? hi : y;
 }
 
+// SBX spread factor (variation.py:77-78) shared by every offspring kernel, so all paths agree bitwise
+__device__ __forceinline__ double sbx_beta_any(double mu, double e) {
+#if !defined(OFF_CUDA_POW) || OFF_CUDA_POW
+    return pow((0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu), e);
+#else
+    return sbx_beta_fast(mu, e);
+#endif
+}
+
 __device__ __forceinline__ void sbx_gene(double x1, double x2, double mu, double swp, double crs,
                                          double e, bool gene_swap, double &c1, double &c2) {
     double beta;
     if (gene_swap && !(crs < 0.5)) {
         beta = 1.0;  // not crossed: masked_blend(crossed, beta, 1)
     } else {
-        beta = (0.5 - mu >= 0.0) ? pow(2.0 * mu, e) : pow(1.0 / (2.0 - 2.0 * mu), e);
+        beta = sbx_beta_any(mu, e);
         if (gene_swap) beta = beta * (1.0 - 2.0 * (swp < 0.5 ? 1.0 : 0.0));
     }
     const double shift = 0.5 * (1.0 - beta);
@@ -337,9 +346,11 @@ constexpr int OW = OFF_OW;  // pairs (warps) per CTA
 // the 4 raw words of stream elements [e, e + 4) where (e - avail) % 4 == 0 (or e < avail)
 __device__ __forceinline__ void raw_quad(const Philox &ph, int64_t e, int64_t avail, uint64_t r[4]) {
     if (e >= avail) {
-        uint64_t c[4];
-        ctr_add(ph.ctr, (uint64_t)((e - avail) >> 2) + 1, c);
-        philox_block(c, ph.key, r);
+        uint64_t c[1][4], o[1][4];
+        ctr_add(ph.ctr, (uint64_t)((e - avail) >> 2) + 1, c[0]);
+        philox_blocks_rk<1>(c, ph.rk, o);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = o[0][k];
     } else {  // head of the stream: buffered words of the host generator (negative e: masked genes)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -360,7 +371,7 @@ __device__ __forceinline__ void raw_quads(const Philox &ph, const int64_t E[NS],
         uint64_t c[NS][4];
 #pragma unroll
         for (int s = 0; s < NS; ++s) ctr_add(ph.ctr, (uint64_t)((E[s] - avail) >> 2) + 1, c[s]);
-        philox_blocks<NS>(c, ph.key, r);
+        philox_blocks_rk<NS>(c, ph.rk, r);
     } else {
 #pragma unroll
         for (int s = 0; s < NS; ++s) raw_quad(ph, E[s], avail, r[s]);
@@ -590,7 +601,7 @@ __global__ void __launch_bounds__(OW * 32, OFF_MINB) k_offspring_w(temo_problem 
 #elif OFF_ABL_POW
                 const double beta0 = (0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu);
 #else
-                const double beta0 = pow((0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu), e);
+                const double beta0 = sbx_beta_any(mu, e);
 #endif
                 const double beta = SWAP ? beta0 * (1.0 - 2.0 * (double)((negate >> k) & 1)) : beta0;
                 const double shift = 0.5 * (1.0 - beta);
@@ -692,6 +703,9 @@ __global__ void __launch_bounds__(OW * 32, OFF_MINB) k_offspring_w(temo_problem 
 #ifndef OFF_FAST_POW
 #define OFF_FAST_POW 0
 #endif
+#ifndef OFF_CUDA_POW
+#define OFF_CUDA_POW 1  // 0: the exp/log form of sbx_pow.cuh (measured no faster on B200)
+#endif
 #ifndef OFF_PREFETCH
 #define OFF_PREFETCH 1
 #endif
@@ -703,7 +717,11 @@ constexpr int SW = 8;            // warps per CTA
 // SBX spread factor of one crossed gene (variation.py:77-78); out of line so pow's
 // internal registers do not inflate the register budget of the offspring kernel
 static __device__ __noinline__ double sbx_beta(double mu, double e) {
+#if OFF_CUDA_POW
     return pow((0.5 - mu >= 0.0) ? 2.0 * mu : 1.0 / (2.0 - 2.0 * mu), e);
+#else
+    return sbx_beta_fast(mu, e);  // exp/log form (sbx_pow.cuh)
+#endif
 }
 constexpr int SMAX_D = 3000;     // genes staged in shared memory (else k_offspring_w)
 
@@ -1525,6 +1543,9 @@ extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation 
         else
             k_offspring_rand<false><<<grid, RW * 32, 0, s>>>(d, V, h, ph, off, 0, beta, flags);
     }
+    TEMO_LAUNCH_CHECK();
+    stage_end(S_OFFSPRING, s);
+    stage_begin(S_OFFSPRING_APPLY, s);
     const size_t sm_a = 3 * d * sizeof(double) + d + 16;
     const unsigned grid = (unsigned)(want < num_sms() * 3 * 8 ? want : num_sms() * 3 * 8);
 #define APPLY_CASE(MM)                                                                              \
@@ -1536,7 +1557,7 @@ extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation 
     TEMO_M_SWITCH(prob->m, APPLY_CASE)
 #undef APPLY_CASE
     TEMO_LAUNCH_CHECK();
-    stage_end(S_OFFSPRING, s);
+    stage_end(S_OFFSPRING_APPLY, s);
     return TEMO_OK;
 }
 

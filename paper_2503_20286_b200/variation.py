@@ -70,6 +70,7 @@ class VariationParams:
         s.eta_c, s.eta_m, s.p_m = self.eta_c, self.eta_m, self.mutation_prob(d)
         s.gene_swap = 1 if self.gene_swap else 0
         s.lower, s.upper = lo_d.data_ptr(), hi_d.data_ptr()
+        s._keep = (lo_d, hi_d)  # the struct owns its bound arrays (no dangling device pointers)
         return s
 
 

@@ -5,9 +5,9 @@ import subprocess
 import sys
 
 
-def main(path, top=40):
-    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+def main(path, top=40, skip=0):
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass",
+                          "--launch-skip", str(skip)], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     fname, recs = "?", []
     hdr = None
@@ -34,4 +34,4 @@ def main(path, top=40):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40, int(sys.argv[3]) if len(sys.argv) > 3 else 0)

@@ -171,8 +171,9 @@ def test_sbx_beta_fast_vs_numpy(cuda):
 
 
 @pytest.mark.parametrize("name,m,d,h,pre", [("lsmop1", 3, 1000, 40, 0), ("lsmop1", 3, 1000, 40, 3),
+                                            ("lsmop1", 3, 1000, 517, 1), ("lsmop1", 5, 700, 33, 2),
                                             ("dtlz1", 3, 12, 50, 1), ("dtlz2", 5, 40, 16, 2),
-                                            ("dtlz7", 3, 13, 3, 0)])
+                                            ("dtlz2", 3, 12, 1000, 3), ("dtlz7", 3, 13, 3, 0)])
 def test_offspring_two_phase_equals_fused(cuda, name, m, d, h, pre):
     """temo_offspring_ws (randomness kernel + streaming apply kernel, the harness path) is
     bit-identical to the fused temo_offspring for every stream alignment (``pre`` shifts the
@@ -196,22 +197,23 @@ def test_offspring_two_phase_equals_fused(cuda, name, m, d, h, pre):
     draws = DeviceDraws(gen)
     off = draws.take(7 * h * d)
     outs = []
-    for two_phase in (False, True):
+    for path in ("fused", "ws-two-phase"):
         O = torch.full((2 * h, d), np.nan, dtype=torch.float64, device=dev)
         FO = torch.full((2 * h, m), np.nan, dtype=torch.float64, device=dev)
         L, s = _lib.lib(), _lib.stream_handle(dev)
         args = (_lib.sptr(prob), _lib.sptr(var), _lib.ptr(X), _lib.ptr(idx), _lib.ptr(idx[h:]), h,
                 _lib.sptr(draws.state), off, _lib.ptr(O), _lib.ptr(FO))
-        if two_phase:
+        if path.startswith("ws"):
             ws = torch.empty(max(L.temo_offspring_ws_bytes(h, d), 256), dtype=torch.uint8, device=dev)
             rc = L.temo_offspring_ws(*args, None, None, _lib.ptr(ws), ws.numel(), s)
         else:
             rc = L.temo_offspring(*args, s)
         assert rc == 0
         outs.append((O.cpu().numpy(), FO.cpu().numpy()))
-    (O1, F1), (O2, F2) = outs
+    (O1, F1) = outs[0]
     assert not np.isnan(O1).any() and not np.isnan(F1).any()
-    assert np.array_equal(O1, O2) and np.array_equal(F1, F2)
+    for O2, F2 in outs[1:]:
+        assert np.array_equal(O1, O2) and np.array_equal(F1, F2)
 
 
 @pytest.mark.parametrize("alg", ["nsga3", "hype"])
