@@ -325,6 +325,12 @@ int temo_hype_select(const double *F, int64_t N, int m, int64_t n, int64_t s, co
                      uint64_t off, const double *U, int32_t *keep, double *v_hv, int32_t *info,
                      void *ws, size_t ws_bytes, temo_stream_t stream);
 
+/* The normalize kernel's np.linalg.solve(E, ones) (nsga3.py:86; OpenBLAS getf2 / blocked
+ * getrf order, bit-exact for m <= 16) on `count` row-major matrices E + E_off[i] of size
+ * m[i] x m[i]; y + y_off[i] receives the solution, ok[i] = 0 on a zero pivot.  Test hook. */
+int temo_lu_solve_batch(const double *E, const int64_t *E_off, const int32_t *m, int64_t count,
+                        double *y, const int64_t *y_off, int32_t *ok, temo_stream_t stream);
+
 /* --------------------------------------------------------------- directions
  * directions.neighbors (directions.py:104-114): out (r x T int32) holds the T
  * nearest rows of W (r x m) by Euclidean distance, ties to the lower index.

@@ -55,6 +55,7 @@ SIGNATURES = {
     "temo_niche_select": (_I32, [_P, _P, _P, _I64, _I32, _P, _I64, _P, _P, _P, _SZ, _P]),
     "temo_update_rank": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _SZ, _P]),
     "temo_gather_rows": (_I32, [_P, _P, _P, _I64, _I64, _P, _P]),
+    "temo_lu_solve_batch": (_I32, [_P, _P, _P, _I64, _P, _P, _P, _P]),
     "temo_gather_rows2": (_I32, [_P, _P, _P, _I64, _I64, _P, _P]),
     "temo_neighbors": (_I32, [_P, _I64, _I32, _I32, _P, _P]),
     "temo_evaluate": (_I32, [_P, _P, _I64, _P, _P]),

@@ -221,38 +221,137 @@ __device__ void jacobi_singular_values(const double *E, int m, double *sv) {
     }
 }
 
-// 1/np.linalg.solve(E, ones) via the App. A4 left-looking LU; returns false if singular
+// np.linalg.solve(E, ones) (nsga3.py:86) bit for bit with NumPy's OpenBLAS 0.3.30 on the
+// SkylakeX kernels (LAPACK dgesv = getrf_single + getrs_N_single), for every m <= 16:
+//   getf2 column j: earlier pivots applied; rows i < j: b_i -= ddot_k(L[i,:i], b) in the
+//     strided ddot order (4-unrolled pairs t1 += fma(y0,x0,y2 x2), t2 += fma(y1,x1,y3 x3),
+//     tail fma chain into t1, t1 + t2); rows i >= j: dgemv_n -- rows of the leading
+//     (rows & ~3) block subtract 4-column groups (acc = a1 x1, fma a0 x0, fma a2 x2, fma a3 x3),
+//     then a 2-column group (fma(a0, x0, a1 x1)), then one column (round(a0 x0)); the last
+//     (rows & 3) rows subtract one fma chain over all columns; first max |b| pivot, rows
+//     swapped over columns 0..j, L scaled by 1/pivot.
+//   getrf_single: blocking = ceil(m/2 / 2) * 2; > 4 (m >= 10) -> panels: getf2 on the panel,
+//     its pivots on the trailing columns, unit-lower TRSM in row blocks 16/8/4/2/1 (GEMM
+//     update from solved rows as an fma chain from 0, then an in-block fma solve), trailing
+//     GEMM (fma chain from 0, one subtraction), later pivots applied to earlier panels.
+//   getrs: laswp, unit-lower axpy substitution, upper substitution with true division.
+// Derived from the library's own kernels (see oracle/csrc/oracle.c, orc_lu_solve, the
+// independent CPU restatement; tests pin both against np.linalg.solve for m = 2..16).
+// Returns false on an exactly zero pivot.
+__device__ double lu_ddot_strided(const double *x, const double *y, int n) {
+    double t1 = 0.0, t2 = 0.0;
+    int i = 0;
+    for (; i + 4 <= n; i += 4) {
+        t1 = t1 + fma(y[i], x[i], y[i + 2] * x[i + 2]);
+        t2 = t2 + fma(y[i + 1], x[i + 1], y[i + 3] * x[i + 3]);
+    }
+    for (; i < n; ++i) t1 = fma(y[i], x[i], t1);
+    return t1 + t2;
+}
+
+__device__ double lu_gemv_row(const double *a, const double *x, int c, double y, bool block_row) {
+    if (!block_row) {
+        double t = 0.0;
+        for (int k = 0; k < c; ++k) t = fma(a[k], x[k], t);
+        return y - t;
+    }
+    int k = 0;
+    for (; k + 4 <= c; k += 4) {
+        double t = a[k + 1] * x[k + 1];
+        t = fma(a[k], x[k], t);
+        t = fma(a[k + 2], x[k + 2], t);
+        t = fma(a[k + 3], x[k + 3], t);
+        y = y - t;
+    }
+    if (c - k >= 2) {
+        y = y - fma(a[k], x[k], a[k + 1] * x[k + 1]);
+        k += 2;
+    }
+    if (c - k == 1) y = y + a[k] * (-x[k]);
+    return y;
+}
+
+// getf2 on rows [r0, m) x columns [c0, c0 + nc) (row-major a, leading dimension MAXM)
+__device__ bool lu_getf2(double (*a)[MAXM], int m, int r0, int c0, int nc, int *ipiv) {
+    const int rows = m - r0;
+    double b[MAXM], lrow[MAXM];
+    for (int jj = 0; jj < nc; ++jj) {
+        const int j = c0 + jj;
+        for (int i = 0; i < rows; ++i) b[i] = a[r0 + i][j];
+        for (int i = 0; i < jj; ++i) {
+            const int jp = ipiv[c0 + i] - r0;
+            if (jp != i) { double t = b[i]; b[i] = b[jp]; b[jp] = t; }
+        }
+        for (int i = 1; i < jj; ++i) {
+            for (int k = 0; k < i; ++k) lrow[k] = a[r0 + i][c0 + k];
+            b[i] = b[i] - lu_ddot_strided(lrow, b, i);
+        }
+        const int rr = rows - jj;
+        if (jj > 0)
+            for (int ii = 0; ii < rr; ++ii) {
+                const int i = jj + ii;
+                for (int k = 0; k < jj; ++k) lrow[k] = a[r0 + i][c0 + k];
+                b[i] = lu_gemv_row(lrow, b, jj, b[i], ii < (rr & ~3));
+            }
+        int jp = jj;
+        double amax = fabs(b[jj]);
+        for (int i = jj + 1; i < rows; ++i)
+            if (fabs(b[i]) > amax) { amax = fabs(b[i]); jp = i; }
+        ipiv[c0 + jj] = r0 + jp;
+        for (int i = 0; i < rows; ++i) a[r0 + i][j] = b[i];
+        if (b[jp] == 0.0) return false;
+        const double rcp = 1.0 / b[jp];
+        if (jp != jj)
+            for (int k = c0; k <= j; ++k) { double t = a[r0 + jj][k]; a[r0 + jj][k] = a[r0 + jp][k]; a[r0 + jp][k] = t; }
+        for (int i = jj + 1; i < rows; ++i) a[r0 + i][j] = a[r0 + i][j] * rcp;
+    }
+    return true;
+}
+
 __device__ bool lu_solve_ones(const double *E, int m, double *y) {
-    double a[MAXM][MAXM], b[MAXM];
+    double a[MAXM][MAXM];
     int ipiv[MAXM];
     for (int i = 0; i < m; ++i)
         for (int j = 0; j < m; ++j) a[i][j] = E[i * m + j];
-    for (int j = 0; j < m; ++j) {
-        for (int i = 0; i < m; ++i) b[i] = a[i][j];
-        for (int i = 0; i < j; ++i)
-            if (ipiv[i] != i) { double t = b[i]; b[i] = b[ipiv[i]]; b[ipiv[i]] = t; }
-        for (int i = 1; i < j; ++i) {
-            double t = a[i][0] * b[0];
-            for (int k = 1; k < i; ++k) t = fma(a[i][k], b[k], t);
-            b[i] = b[i] - t;
+    const int blocking = ((m / 2 + 1) / 2) * 2;
+    if (blocking <= 4) {
+        if (!lu_getf2(a, m, 0, 0, m, ipiv)) return false;
+    } else {
+        for (int j = 0; j < m; j += blocking) {
+            const int jmin = m - j < blocking ? m - j : blocking;
+            if (!lu_getf2(a, m, j, j, jmin, ipiv)) return false;
+            if (j + jmin >= m) continue;
+            for (int c = j + jmin; c < m; ++c)
+                for (int i = j; i < j + jmin; ++i)
+                    if (ipiv[i] != i) { double t = a[i][c]; a[i][c] = a[ipiv[i]][c]; a[ipiv[i]][c] = t; }
+            int bstart[8], bsize[8], nb = 0, r0 = 0, rem = jmin;
+            for (int bs = 16; bs >= 1; bs >>= 1)
+                while (rem >= bs) { bstart[nb] = r0; bsize[nb++] = bs; r0 += bs; rem -= bs; }
+            for (int c = j + jmin; c < m; ++c)
+                for (int q = 0; q < nb; ++q) {
+                    const int b0 = j + bstart[q], b1 = b0 + bsize[q];
+                    if (bstart[q] > 0)
+                        for (int i = b0; i < b1; ++i) {
+                            double acc = 0.0;
+                            for (int k = j; k < b0; ++k) acc = fma(a[i][k], a[k][c], acc);
+                            a[i][c] = a[i][c] - acc;
+                        }
+                    for (int i = b0; i < b1; ++i)
+                        for (int k = i + 1; k < b1; ++k) a[k][c] = fma(-a[i][c], a[k][i], a[k][c]);
+                }
+            for (int i = j + jmin; i < m; ++i)
+                for (int c = j + jmin; c < m; ++c) {
+                    double acc = 0.0;
+                    for (int k = j; k < j + jmin; ++k) acc = fma(a[i][k], a[k][c], acc);
+                    a[i][c] = a[i][c] - acc;
+                }
         }
-        if (j > 0)
-            for (int i = j; i < m; ++i) {
-                double t = a[i][0] * b[0];
-                for (int k = 1; k < j; ++k) t = fma(a[i][k], b[k], t);
-                b[i] = b[i] - t;
-            }
-        int jp = j;
-        double amax = fabs(b[j]);
-        for (int i = j + 1; i < m; ++i)
-            if (fabs(b[i]) > amax) { amax = fabs(b[i]); jp = i; }
-        ipiv[j] = jp;
-        for (int i = 0; i < m; ++i) a[i][j] = b[i];
-        if (jp != j)
-            for (int k = 0; k <= j; ++k) { double t = a[j][k]; a[j][k] = a[jp][k]; a[jp][k] = t; }
-        if (a[j][j] == 0.0) return false;
-        const double r = 1.0 / a[j][j];
-        for (int i = j + 1; i < m; ++i) a[i][j] = a[i][j] * r;
+        for (int j = 0; j < m; j += blocking) {
+            const int jmin = m - j < blocking ? m - j : blocking;
+            for (int i = j + jmin; i < m; ++i)
+                if (ipiv[i] != i)
+                    for (int c = j; c < j + jmin; ++c) { double t = a[i][c]; a[i][c] = a[ipiv[i]][c]; a[ipiv[i]][c] = t; }
+        }
     }
     for (int i = 0; i < m; ++i) y[i] = 1.0;
     for (int i = 0; i < m; ++i)
@@ -264,6 +363,22 @@ __device__ bool lu_solve_ones(const double *E, int m, double *y) {
         for (int k = 0; k < i; ++k) y[k] = fma(-y[i], a[k][i], y[k]);
     }
     return true;
+}
+
+// one thread per matrix: the normalize kernel's solve on caller matrices (temo_lu_solve_batch)
+__global__ void k_lu_batch(const double *__restrict__ E, const int64_t *__restrict__ E_off,
+                           const int32_t *__restrict__ ms, int64_t count, double *__restrict__ y,
+                           const int64_t *__restrict__ y_off, int32_t *__restrict__ ok) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const int m = ms[i];
+    if (m < 1 || m > MAXM) {
+        ok[i] = 0;
+        return;
+    }
+    double yy[MAXM];
+    ok[i] = lu_solve_ones(E + E_off[i], m, yy) ? 1 : 0;
+    for (int k = 0; k < m; ++k) y[y_off[i] + k] = yy[k];
 }
 
 // single thread: extremes -> E -> gate -> intercepts (nsga3.py:84-93)
@@ -1056,6 +1171,15 @@ extern "C" int temo_gather_rows2(const double *src, const int64_t *idx_a, const 
     if (rows == 0) return TEMO_OK;
     cudaStream_t st = (cudaStream_t)stream;
     k_gather_rows2<<<g1(rows * 32), NT, 0, st>>>(src, idx_a, idx_b, rows, cols, dst);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
+extern "C" int temo_lu_solve_batch(const double *E, const int64_t *E_off, const int32_t *m, int64_t count,
+                                   double *y, const int64_t *y_off, int32_t *ok, temo_stream_t stream) {
+    if (count < 0 || (count && (!E || !E_off || !m || !y || !y_off || !ok))) return TEMO_EINVAL;
+    if (!count) return TEMO_OK;
+    k_lu_batch<<<(unsigned)((count + 127) / 128), 128, 0, (cudaStream_t)stream>>>(E, E_off, m, count, y, y_off, ok);
     TEMO_LAUNCH_CHECK();
     return TEMO_OK;
 }

@@ -168,6 +168,16 @@ def gen_nsga3():
     spec2 = problems.make_problem("dtlz2", m=3)
     Fm = problems.evaluate(spec2, r.random((1200, spec2.d)))
     cases.append(selection_case(Fm, np.zeros((1200, 1)), directions.das_dennis(3, 33), 600, r.permutation(1200)))
+    # many objectives with well-conditioned extremes: the hyperplane (np.linalg.solve) branch at
+    # m = 6, 8, 10 (OpenBLAS getf2) and 12 (blocked getrf), not the nadir fallback
+    for k, (N, m, H, n) in enumerate(((400, 6, 4, 200), (400, 8, 3, 200), (360, 10, 3, 180), (300, 12, 2, 150))):
+        r2 = np.random.default_rng(500 + k)
+        Fm = r2.dirichlet(np.ones(m), N) * (1.0 + 0.5 * r2.random((N, 1))) + 1e-3 * r2.random((N, m))
+        c = selection_case(Fm, np.zeros((N, 1)), directions.das_dennis(m, H), n, r2.permutation(N))
+        live = c["r"] <= c["l"]
+        fallback = np.maximum(np.nanmax(Fm[c["perm"]][live], axis=0), 1e-10)
+        assert not np.array_equal(c["intercepts"], fallback), "expected the solve branch"
+        cases.append(c)
     # degenerate extremes -> fallback intercepts
     Fm = np.repeat(np.array([[1.0, 1.0, 1.0], [2.0, 2.0, 2.0]]), 30, axis=0) + np.linspace(0, 1e-3, 60)[:, None]
     cases.append(selection_case(Fm, np.zeros((60, 1)), directions.das_dennis(3, 4), 30, r.permutation(60)))
@@ -180,13 +190,18 @@ def gen_nsga3():
 
 
 def gen_linalg():
+    """np.linalg.solve(E, ones) bits (nsga3.py:86) for m = 2..16: random and NSGA-III-shaped E
+    (extreme points of shifted objectives: nonnegative, dominant diagonal).  m <= 9 is OpenBLAS's
+    unblocked getf2; m >= 10 its blocked getrf_single."""
     r = np.random.default_rng(300)
     Es, ys, ms = [], [], []
-    for _ in range(3000):
-        m = int(r.integers(2, 6))
+    for k in range(3000 + 15 * 240):
+        m = int(r.integers(2, 6)) if k < 3000 else 2 + (k - 3000) // 240
         E = r.random((m, m)) * r.choice([1e-3, 1.0, 1e3])
         if r.random() < 0.3:
             E = E + np.diag(r.random(m)) * 5
+        if k >= 3000 and (k % 3) == 0:  # extreme-point shaped: near-diagonal, scaled axes
+            E = np.diag(1.0 + r.random(m) * 10) + r.random((m, m)) * 1e-3 * r.choice([1.0, 10.0, 100.0])
         Es.append(E)
         ys.append(np.linalg.solve(E, np.ones(m)))
         ms.append(m)
@@ -341,7 +356,10 @@ def gen_config_a():
 
 
 if __name__ == "__main__":
+    wanted = set(sys.argv[1:])  # e.g. "gen_linalg": regenerate only those sets
     for fn in (gen_ndsort, gen_nsga3, gen_linalg, gen_associate, gen_hype, gen_variation, gen_problems,
                gen_moead, gen_neighbors, gen_config_a):
+        if wanted and fn.__name__ not in wanted:
+            continue
         fn()
         print("wrote", fn.__name__)

@@ -18,7 +18,7 @@ class Planned:
         return self.perm.copy()
 
 
-@pytest.mark.parametrize("idx", range(14))
+@pytest.mark.parametrize("idx", range(18))
 def test_selection_golden_stages(cuda, idx):
     import torch
 
@@ -40,7 +40,13 @@ def test_selection_golden_stages(cuda, idx):
     live = c["r"] <= l
     assert np.array_equal(sel.Fp.cpu().numpy()[live], c["Fp"][live])
     assert np.array_equal(sel.pi.cpu().numpy()[live], c["pi"][live])
-    assert np.array_equal(sel.dist.cpu().numpy()[live], c["dist"][live])
+    # distances bit-exact for m <= 4; for m >= 5 OpenBLAS's dgemm computes the last (n_r mod 8)
+    # direction columns in an edge kernel whose order is not restated: within
+    # the north star's tolerance there, association indices still exact
+    if m <= 4:
+        assert np.array_equal(sel.dist.cpu().numpy()[live], c["dist"][live])
+    else:
+        assert np.allclose(sel.dist.cpu().numpy()[live], c["dist"][live], rtol=1e-12, atol=0)
     k = int(sel.counts[0].item())
     assert np.array_equal(sel.promoted[:k].cpu().numpy(), c["promoted"])
     assert np.array_equal(keep, c["keep"])
@@ -253,3 +259,28 @@ def test_failed_selection_leaves_valid_keep_and_pool(cuda):
                                      _lib.ptr(sel.status), _lib.ptr(ws), ws.numel(), _lib.stream_handle(cuda))
     assert rc == 0
     assert torch.equal(out, phys)
+
+
+def test_intercept_solve_lapack_bits_all_m(cuda):
+    """The normalize kernel's solve (nsga3.py:86) equals np.linalg.solve bit for bit for m = 2..16
+    (OpenBLAS getf2 order for m <= 9, blocked getrf for m >= 10) on the reference-generated
+    golden matrices (tests/golden/linalg.npz)."""
+    import torch
+
+    from paper_2503_20286_b200 import _lib
+
+    z = dict(load_golden("linalg"))
+    ms = z["m"].astype(np.int32)
+    E = torch.from_numpy(z["E"]).cuda()
+    Eo = torch.from_numpy(z["E_off"][:-1].astype(np.int64)).cuda()
+    yo = torch.from_numpy(z["y_off"][:-1].astype(np.int64)).cuda()
+    y = torch.zeros(len(z["y"]), dtype=torch.float64, device=cuda)
+    ok = torch.zeros(len(ms), dtype=torch.int32, device=cuda)
+    rc = _lib.lib().temo_lu_solve_batch(_lib.ptr(E), _lib.ptr(Eo), _lib.ptr(torch.from_numpy(ms).cuda()), len(ms),
+                                        _lib.ptr(y), _lib.ptr(yo), _lib.ptr(ok), _lib.stream_handle(cuda))
+    assert rc == 0
+    got = y.cpu().numpy()
+    assert ok.cpu().numpy().all()
+    bad = [int(ms[i]) for i in range(len(ms)) if not np.array_equal(got[z["y_off"][i]:z["y_off"][i + 1]],
+                                                                     z["y"][z["y_off"][i]:z["y_off"][i + 1]])]
+    assert not bad, f"mismatches at m = {sorted(set(bad))}"
