@@ -331,6 +331,41 @@ int temo_hype_select(const double *F, int64_t N, int m, int64_t n, int64_t s, co
 int temo_lu_solve_batch(const double *E, const int64_t *E_off, const int32_t *m, int64_t count,
                         double *y, const int64_t *y_off, int32_t *ok, temo_stream_t stream);
 
+/* ---------------------------------------------------------------- indicators
+ * indicators.py:19-100 on the device (csrc/indicators.cu); `out` is one device double.
+ * temo_igd : mean over the r reference points Fstar of the distance to the nearest of the
+ *            n rows of F (NumPy's last-axis sum and pairwise mean order).
+ * temo_hv  : exact dominated volume for m = 2, 3 (sweep / z-slab decomposition, NumPy's
+ *            summation orders); rows with any coordinate >= ref are dropped.  Reads two
+ *            counts back to the host (data-dependent slab count).
+ * temo_hv_mc_hits : m > 3 Monte-Carlo part: hits[s] = 1 iff some row of F <= S[s].
+ * temo_eu  : expected utility of U (= -F when minimising) under r weight rows (best
+ *            weighted utility per row, or the per-objective `literal` reading), mean. */
+size_t temo_igd_ws_bytes(int64_t r);
+int temo_igd(const double *F, int64_t n, int m, const double *Fstar, int64_t r, double *out, void *ws,
+             size_t ws_bytes, temo_stream_t stream);
+size_t temo_hv_ws_bytes(int64_t n, int m);
+int temo_hv(const double *F, int64_t n, int m, const double *ref, double *out, void *ws, size_t ws_bytes,
+            temo_stream_t stream);
+int temo_hv_mc_hits(const double *F, int64_t n, int m, const double *S, int64_t ns, int32_t *hits,
+                    temo_stream_t stream);
+size_t temo_eu_ws_bytes(int64_t n, int64_t r, int literal);
+int temo_eu(const double *U, int64_t n, int m, const double *W, int64_t r, int literal, double *out, void *ws,
+            size_t ws_bytes, temo_stream_t stream);
+
+/* -------------------------------------------------------------------- RVEA
+ * rvea.apd_select (rvea.py:33-68).  temo_rvea_prep: unit directions Vn (r x m) and the
+ * minimal inter-direction angles gamma (r) of W.  temo_rvea_select: one elite per non-empty
+ * angle partition of F (N x m) by smallest angle-penalized distance, winners in direction
+ * order into keep (<= r, int32 row indices), their number into *count (device);
+ * mp = m * (t / t_max)^alpha.  part_out / apd_out (nullable) receive every row's partition
+ * and APD. */
+int temo_rvea_prep(const double *W, int64_t r, int m, double *Vn, double *gamma, temo_stream_t stream);
+size_t temo_rvea_select_ws_bytes(int64_t N, int m, int64_t r);
+int temo_rvea_select(const double *F, int64_t N, int m, const double *Vn, const double *gamma, int64_t r,
+                     double mp, int32_t *keep, int32_t *count, int32_t *part_out, double *apd_out, void *ws,
+                     size_t ws_bytes, temo_stream_t stream);
+
 /* --------------------------------------------------------------- directions
  * directions.neighbors (directions.py:104-114): out (r x T int32) holds the T
  * nearest rows of W (r x m) by Euclidean distance, ties to the lower index.

@@ -56,6 +56,16 @@ SIGNATURES = {
     "temo_update_rank": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P, _P, _SZ, _P]),
     "temo_gather_rows": (_I32, [_P, _P, _P, _I64, _I64, _P, _P]),
     "temo_lu_solve_batch": (_I32, [_P, _P, _P, _I64, _P, _P, _P, _P]),
+    "temo_rvea_prep": (_I32, [_P, _I64, _I32, _P, _P, _P]),
+    "temo_rvea_select_ws_bytes": (_SZ, [_I64, _I32, _I64]),
+    "temo_rvea_select": (_I32, [_P, _I64, _I32, _P, _P, _I64, _D, _P, _P, _P, _P, _P, _SZ, _P]),
+    "temo_igd_ws_bytes": (_SZ, [_I64]),
+    "temo_igd": (_I32, [_P, _I64, _I32, _P, _I64, _P, _P, _SZ, _P]),
+    "temo_hv_ws_bytes": (_SZ, [_I64, _I32]),
+    "temo_hv": (_I32, [_P, _I64, _I32, _P, _P, _P, _SZ, _P]),
+    "temo_hv_mc_hits": (_I32, [_P, _I64, _I32, _P, _I64, _P, _P]),
+    "temo_eu_ws_bytes": (_SZ, [_I64, _I64, _I32]),
+    "temo_eu": (_I32, [_P, _I64, _I32, _P, _I64, _I32, _P, _P, _SZ, _P]),
     "temo_gather_rows2": (_I32, [_P, _P, _P, _I64, _I64, _P, _P]),
     "temo_neighbors": (_I32, [_P, _I64, _I32, _I32, _P, _P]),
     "temo_evaluate": (_I32, [_P, _P, _I64, _P, _P]),

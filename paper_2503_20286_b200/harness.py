@@ -20,21 +20,27 @@ from __future__ import annotations
 
 import ctypes
 import dataclasses
+import json
 import math
+import platform
 import time
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 
 from . import _lib
 from .directions import DirectionSet, das_dennis, largest_h_for, neighbors
+from .indicators import hv_indicator, igd
 from .nsga3 import Nsga3Selector
-from .problems import ProblemSpec, make_problem
+from .problems import ProblemSpec, make_problem, true_front
 from .rng import DeviceDraws, RngStream
 from .rng import permutation as rng_permutation
 from .variation import VariationParams
 
-ALGORITHMS = ("nsga3", "moead", "hype")
+ALGORITHMS = ("nsga3", "moead", "hype", "rvea")
+HOST_ONLY = ("nsga3-seq", "moead-seq")  # the reference's sequential baselines (baselines.py)
+CSV_COLUMNS = ("generation", "time_s", "igd", "hv")
 
 
 class ConfigError(ValueError):
@@ -43,7 +49,8 @@ class ConfigError(ValueError):
 
 @dataclass(frozen=True)
 class RunConfig:
-    """Everything needed to reproduce one experiment (harness.py:39-82 field names)."""
+    """Everything needed to reproduce one experiment (harness.py:39-82: same fields, defaults and
+    validation) plus ``aggregation`` (MOEA/D "pbi" | "tch") and ``device``."""
 
     algorithm: str = "nsga3"
     problem: str = "dtlz2"
@@ -59,21 +66,47 @@ class RunConfig:
     theta: float = 5.0
     neighborhood: int | None = None
     divisions: int | None = None
+    alpha: float = 2.0
     hv_samples: int | None = None
     hv_ref: str = "auto"
+    indicators: tuple = ("igd", "hv")
+    indicator_every: int = 1
+    ref_front_size: int = 1000
     time_selection_only: bool = False
+    out: str | None = None
     aggregation: str = "pbi"  # MOEA/D: "pbi" (reference) or "tch" (Tchebycheff, new)
     device: str | None = None
 
     def validate(self) -> None:
         if self.algorithm not in ALGORITHMS:
+            if self.algorithm in HOST_ONLY:
+                raise ConfigError(f"{self.algorithm!r} is the reference's sequential CPU baseline, "
+                                  "not part of the GPU hot path")
             raise ConfigError(f"unknown algorithm {self.algorithm!r}")
         if self.objectives < 2 or self.pop_size < 2 or self.repeats < 1:
             raise ConfigError("objectives >= 2, pop-size >= 2, repeats >= 1 required")
-        if self.generations < 0:
-            raise ConfigError("generations must be non-negative")
+        if self.generations < 0 or self.indicator_every < 0:
+            raise ConfigError("generations and indicator-every must be non-negative")
+        if self.ref_front_size < self.objectives:
+            raise ConfigError("ref-front-size must be at least the objective count")
+        for name in self.indicators:
+            if name not in ("igd", "hv", "eu"):
+                raise ConfigError(f"unknown indicator {name!r}")
+        if self.hv_ref != "auto":
+            try:
+                _parse_ref_vector(self.hv_ref, self.objectives)
+            except ValueError as exc:
+                raise ConfigError(str(exc)) from None
         if self.aggregation not in ("pbi", "tch"):
             raise ConfigError(f"unknown aggregation {self.aggregation!r}")
+
+
+def _parse_ref_vector(text: str, m: int) -> np.ndarray:
+    """harness.py:85-89."""
+    parts = [float(v) for v in str(text).split(",")]
+    if len(parts) != m:
+        raise ValueError(f"hv-ref needs {m} comma-separated values")
+    return np.asarray(parts)
 
 
 def _resolve(config: RunConfig):
@@ -88,7 +121,7 @@ def _resolve(config: RunConfig):
             raise ConfigError("pop-size below objective count leaves no directions")
         H = largest_h_for(config.pop_size, config.objectives)
     R = das_dennis(config.objectives, H)
-    n_eff = R.count if config.algorithm == "moead" else config.pop_size
+    n_eff = R.count if config.algorithm in ("moead", "rvea") else config.pop_size
     return spec, R, n_eff
 
 
@@ -169,6 +202,10 @@ class _Stepper:
                 [float(v) for v in str(config.hv_ref).split(",")])
             s = config.hv_samples or 10 * n
             self.selector = HypeSelector(self.N, m, n, s, ref, self.dev)
+        elif alg == "rvea":
+            from .rvea import RveaSelector
+
+            self.selector = RveaSelector(self.N, m, R, config.alpha, self.dev)
         elif alg == "moead":
             from .moead import MoeadEngine, default_neighborhood
 
@@ -201,42 +238,64 @@ class _Stepper:
             st.extra["moead"] = self.engine.init_state(cur.X[: self.n], cur.F[: self.n])
         return st
 
-    # -- offspring of NSGA-III / HypE (harness.py:201-204, 218-222) into rows [n, N)
+    # -- offspring of NSGA-III / HypE / RVEA (harness.py:201-204, 218-222) into rows [n, N)
     def _offspring(self, st: DeviceState, gen):
-        i1, i2 = (lambda p, h: (p[:h], p[h: 2 * h]))(rng_permutation(gen, self.n), self.h)
-        self.ring.upload(np.concatenate([i1, i2]).astype(np.int64), self.i12)
+        n = st.n  # RVEA's population is the number of non-empty partitions (<= self.n)
+        if n < 2:
+            return self._mutate_in_place(st, gen)
+        h = n // 2
+        i1, i2 = (lambda p, hh: (p[:hh], p[hh: 2 * hh]))(rng_permutation(gen, n), h)
+        self.ring.upload(np.concatenate([i1, i2]).astype(np.int64), self.i12[: 2 * h])
         draws = DeviceDraws(gen)
-        hd = self.h * self.spec.d
+        hd = h * self.spec.d
         off = draws.take((3 if self.params.gene_swap else 1) * hd + 4 * hd)
         cur = st.cur
-        pooled = ((self.h * self.spec.d) % 4 == 0 and self.spec.d <= 3000  # two-phase path (row maps)
+        pooled = ((h * self.spec.d) % 4 == 0 and self.spec.d <= 3000  # two-phase path (row maps)
                   and not getattr(self, "force_unpooled", False))
         if pooled:
-            src, dst, obase = _lib.ptr(st.phys), _lib.ptr(st.phys[self.n:]), _lib.ptr(cur.X)
+            src, dst, obase = _lib.ptr(st.phys), _lib.ptr(st.phys[n:]), _lib.ptr(cur.X)
         else:  # fused fallback: children into logical rows; make the pool the identity first
             self._pool_identity(st)
-            src, dst, obase = None, None, _lib.ptr(cur.X[self.n:])
+            src, dst, obase = None, None, _lib.ptr(cur.X[n:])
         rc = _lib.lib().temo_offspring_ws(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
-                                          _lib.ptr(self.i12), _lib.ptr(self.i12[self.h:]), self.h,
+                                          _lib.ptr(self.i12), _lib.ptr(self.i12[h:]), h,
                                           _lib.sptr(draws.state), off, obase,
-                                          _lib.ptr(cur.F[self.n:]), src, dst,
+                                          _lib.ptr(cur.F[n:]), src, dst,
                                           _lib.ptr(self.off_ws), self.off_ws.numel(),
                                           _lib.stream_handle(self.dev))
         _lib.check(rc, "offspring")
         draws.commit()
+        st.extra["N_cur"] = n + 2 * h
+
+    def _mutate_in_place(self, st: DeviceState, gen):
+        """A shrunken population of one row: O = polynomial_mutation(X) (harness.py:223-226)."""
+        from .problems import evaluate_device
+
+        n, d = st.n, self.spec.d
+        self._pool_identity(st)
+        draws = DeviceDraws(gen)
+        off = draws.take(2 * n * d)  # mu then hit (variation.py:107-108)
+        X = st.cur.X
+        rc = _lib.lib().temo_pm(_lib.sptr(self.var), _lib.ptr(X[:n]), n, d, _lib.sptr(draws.state), off,
+                                None, None, _lib.ptr(X[n: 2 * n]), _lib.stream_handle(self.dev))
+        _lib.check(rc, "polynomial_mutation")
+        draws.commit()
+        evaluate_device(self.spec, X[n: 2 * n], out=st.cur.F[n: 2 * n])
+        st.extra["N_cur"] = 2 * n
 
     def _pool_identity(self, st: DeviceState):
         """Materialise the parents into pool rows [0, n) (fused-offspring fallback only)."""
         if st.phys is not None and st.extra.get("pool_identity") is not True:
-            X = st.rows(0, self.n)
-            st.cur.X[: self.n].copy_(X)
+            X = st.rows(0, st.n)
+            st.cur.X[: st.n].copy_(X)
             st.phys.copy_(_lib.torch().arange(self.N, dtype=_lib.torch().int64, device=self.dev))
         st.extra["pool_identity"] = True
 
-    def _pool_update(self, st: DeviceState, perm, keep):
+    def _pool_update(self, st: DeviceState, perm, keep, n_new: int | None = None):
         """phys' = survivors' pool rows, then the freed rows (temo_pool_update)."""
+        n_new = self.n if n_new is None else n_new
         out = self.phys[1] if st.phys.data_ptr() == self.phys[0].data_ptr() else self.phys[0]
-        rc = _lib.lib().temo_pool_update(_lib.ptr(st.phys), _lib.ptr(perm), _lib.ptr(keep), self.N, self.n,
+        rc = _lib.lib().temo_pool_update(_lib.ptr(st.phys), _lib.ptr(perm), _lib.ptr(keep), self.N, n_new,
                                          _lib.ptr(out), _lib.ptr(self.selector.status),
                                          _lib.ptr(self.pool_ws), self.pool_ws.numel(),
                                          _lib.stream_handle(self.dev))
@@ -246,29 +305,53 @@ class _Stepper:
 
     def offspring_rows(self, st: DeviceState):
         """X of the current offspring (logical rows [n, N))."""
-        return st.rows(self.n, self.N)
+        return st.rows(st.n, st.extra.get("N_cur", self.N))
 
-    def step(self, st: DeviceState, g: int, gen):
+    def step(self, st: DeviceState, g: int, gen, timed: bool = True):
+        """One generation (harness.py:206-248); returns (state, seconds).
+
+        ``seconds`` is the device time of the whole step -- or of the selection alone with
+        ``time_selection_only`` -- from CUDA events on the launching stream (the call waits for
+        the step).  ``timed=False`` returns at once with ``seconds = None`` (launch-ahead loops)."""
+        t = _lib.torch()
         alg = self.config.algorithm
-        t0 = time.perf_counter()
+        ev = [t.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
+        if timed:
+            ev[0].record()
         if alg == "moead":
             st.extra["moead"] = self.engine.step(st.extra["moead"], gen)
-            return st, time.perf_counter() - t0
-        self._offspring(st, gen)
-        ts = time.perf_counter()
-        cur, nxt = st.cur, st.nxt
-        n = self.n
-        if alg == "nsga3":
-            self.ring.upload(rng_permutation(gen, self.N), self.perm)
-            keep = self.selector.select(cur.F, self.perm)
-            self._pool_update(st, self.perm, keep)  # survivors' X rows stay where they are
-            _lib.gather_rows(self.selector.Fs, keep, nxt.F[:n])
-        else:  # hype (no shuffle; hype.py:135-163)
-            keep = self.selector.select(cur.F, gen)
-            self._pool_update(st, None, keep)
-            _lib.gather_rows(cur.F, keep, nxt.F[:n])
-        st.cur, st.nxt = nxt, cur
-        return st, time.perf_counter() - ts
+            if timed:
+                ev[1].record()
+                ev[2].record()
+        else:
+            self._offspring(st, gen)
+            if timed:
+                ev[1].record()
+            cur, nxt = st.cur, st.nxt
+            n = self.n
+            if alg == "nsga3":
+                self.ring.upload(rng_permutation(gen, self.N), self.perm)
+                keep = self.selector.select(cur.F, self.perm)
+                self._pool_update(st, self.perm, keep)  # survivors' X rows stay where they are
+                _lib.gather_rows(self.selector.Fs, keep, nxt.F[:n])
+            elif alg == "hype":  # no shuffle (hype.py:135-163)
+                keep = self.selector.select(cur.F, gen)
+                self._pool_update(st, None, keep)
+                _lib.gather_rows(cur.F, keep, nxt.F[:n])
+            else:  # rvea: apd_select over [parents; offspring] (rvea.py:33-68, harness.py:240-244)
+                keep = self.selector.select(cur.F, g, max(self.config.generations, 1), st.extra["N_cur"])
+                k = int(keep.shape[0])
+                self._pool_update(st, None, keep, k)
+                _lib.gather_rows(cur.F, keep, nxt.F[:k])
+                st.n = k
+            st.cur, st.nxt = nxt, cur
+            if timed:
+                ev[2].record()
+        if not timed:
+            return st, None
+        ev[2].synchronize()
+        first = 1 if self.config.time_selection_only else 0
+        return st, ev[first].elapsed_time(ev[2]) * 1e-3
 
     def check(self):
         """Raise the reference's exception if a selection failed (device status word)."""
@@ -290,41 +373,227 @@ class _Stepper:
 
 @dataclass
 class GenRow:
+    """harness.py:92-98."""
+
     generation: int
     time_s: float
+    igd: float
+    hv: float
     ideal: list
 
 
 @dataclass
+class RepeatRecord:
+    """harness.py:101-110."""
+
+    repeat: int
+    initial: dict
+    rows: list = field(default_factory=list)
+    mean_gen_time_s: float = math.nan
+    final_igd: float = math.nan
+    final_hv: float = math.nan
+    timed_out: bool = False
+
+
+@dataclass
 class RunRecord:
+    """harness.py:113-118."""
+
     config: dict
-    rows: list
+    metadata: dict
+    repeats: list
+    summary: dict
+
+
+@dataclass
+class ScaleCell:
+    size: int
     mean_gen_time_s: float
-    final_F: np.ndarray
+    generations_done: int
+    status: str  # "ok" | "timeout"
 
 
-def run(config: RunConfig, sync_every_step: bool = True) -> RunRecord:
-    """Execute one repeat of a configured run (harness.py:270-319, timing per generation).
+@dataclass
+class ScaleResult:
+    kind: str
+    config: dict
+    metadata: dict
+    cells: list
 
-    Each generation is timed from launch to the host read of the new ideal
-    point (the reference records ``F.min(axis=0)`` per generation)."""
+
+def _metadata() -> dict:
+    from . import __version__
+
+    t = _lib.torch()
+    dev = t.cuda.get_device_name(t.cuda.current_device()) if t.cuda.is_available() else "none"
+    return {"library": f"temo {__version__} (paper_2503_20286_b200)", "platform": platform.platform(),
+            "python": platform.python_version(), "numpy": np.__version__, "device": dev}
+
+
+class _Indicators:
+    """Cached reference front and HV corner for per-generation metrics (harness.py:250-268);
+    the indicators themselves run on the device (indicators.py)."""
+
+    def __init__(self, config: RunConfig, spec: ProblemSpec):
+        self.want_igd = "igd" in config.indicators
+        self.want_hv = "hv" in config.indicators
+        self.front = None
+        self.hv_ref = None
+        if self.want_igd or self.want_hv:
+            self.front = true_front(spec, config.ref_front_size)
+            self.hv_ref = 1.1 * self.front.max(axis=0)
+            self.hv_ref[self.hv_ref <= 0] = 1e-6
+            self.front_d = _lib.torch().from_numpy(np.ascontiguousarray(self.front)).to(_lib.device(config.device))
+
+    def measure(self, F) -> tuple:
+        gi = igd(F, self.front_d) if self.want_igd else math.nan
+        gh = hv_indicator(F, self.hv_ref) if self.want_hv else math.nan
+        return gi, gh
+
+
+def run(config: RunConfig, deadline: float | None = None) -> RunRecord:
+    """Execute all repeats of a configured run (harness.py:270-319), optionally up to a deadline.
+
+    Every generation's ``time_s`` is the device time of the step (or of the selection with
+    ``time_selection_only``) from CUDA events; indicators run on the device every
+    ``indicator_every`` generations; ``ideal`` is the objective-wise minimum (one host read per
+    generation, as the reference records it).  The device status word is checked every
+    generation, so a failed selection raises the reference's exception at once."""
     config.validate()
     spec, R, n_eff = _resolve(config)
     stepper = _Stepper(config, spec, R, n_eff)
-    gen = RngStream(config.seed).split(0).generator()
-    st = stepper.init(gen)
-    rows = []
-    for g in range(1, config.generations + 1):
-        t0 = time.perf_counter()
-        st, sel_s = stepper.step(st, g, gen)
+    metrics = _Indicators(config, spec)
+    root = RngStream(config.seed)
+    repeats = []
+    for rep in range(config.repeats):
+        gen = root.split(rep).generator()
+        st = stepper.init(gen)
         F = stepper.objectives(st)
-        ideal = F.min(dim=0).values.cpu().numpy().tolist() if sync_every_step else []
-        total = time.perf_counter() - t0
-        if sync_every_step:
+        gi, gh = metrics.measure(F)
+        record = RepeatRecord(rep, {"igd": gi, "hv": gh, "ideal": F.min(dim=0).values.cpu().numpy().tolist()})
+        for g in range(1, config.generations + 1):
+            st, time_s = stepper.step(st, g, gen)
             stepper.check()
-        rows.append(GenRow(g, sel_s if config.time_selection_only else total, ideal))
-    F = stepper.objectives(st)
-    Fh = F.cpu().numpy()
-    stepper.check()
-    mean = float(np.mean([r.time_s for r in rows])) if rows else math.nan
-    return RunRecord(dataclasses.asdict(config), rows, mean, Fh)
+            F = stepper.objectives(st)
+            every = config.indicator_every
+            if every > 0 and g % every == 0:
+                gi, gh = metrics.measure(F)
+            else:
+                gi, gh = math.nan, math.nan
+            record.rows.append(GenRow(g, time_s, gi, gh, F.min(dim=0).values.cpu().numpy().tolist()))
+            if deadline is not None and time.perf_counter() > deadline:
+                record.timed_out = True
+                break
+        F = stepper.objectives(st)
+        record.final_igd, record.final_hv = metrics.measure(F)
+        if record.rows:
+            record.mean_gen_time_s = float(np.mean([r.time_s for r in record.rows]))
+        repeats.append(record)
+        if deadline is not None and time.perf_counter() > deadline:
+            break
+    summary = {
+        "median_final_igd": float(np.median([r.final_igd for r in repeats])),
+        "median_final_hv": float(np.median([r.final_hv for r in repeats])),
+        "mean_gen_time_s": float(np.mean([r.mean_gen_time_s for r in repeats])),
+        "effective_pop_size": n_eff,
+        "directions": R.count,
+    }
+    rec = RunRecord(dataclasses.asdict(config), _metadata(), repeats, summary)
+    if config.out:
+        emit(rec, "json", config.out)
+    return rec
+
+
+def scaling_experiment(kind: str, base: RunConfig, steps: int, timeout_s: float | None = None) -> ScaleResult:
+    """Double the population or the dimension per step and time each cell (harness.py:322-361)."""
+    if kind not in ("population", "dimension"):
+        raise ConfigError("scale kind must be 'population' or 'dimension'")
+    if steps < 1:
+        raise ConfigError("steps must be at least 1")
+    base.validate()
+    cells = []
+    for step_idx in range(steps):
+        if kind == "population":
+            size = base.pop_size * (2 ** step_idx)
+            cfg = dataclasses.replace(base, pop_size=size, out=None)
+        else:
+            start = base.dim if base.dim is not None else 1024
+            size = start * (2 ** step_idx)
+            cfg = dataclasses.replace(base, dim=size, out=None)
+        dl = None if timeout_s is None else time.perf_counter() + timeout_s
+        record = run(cfg, deadline=dl)
+        timed_out = any(r.timed_out for r in record.repeats) or len(record.repeats) < cfg.repeats
+        done = sum(len(r.rows) for r in record.repeats)
+        if timed_out:
+            cells.append(ScaleCell(size, math.nan, done, "timeout"))
+        else:
+            cells.append(ScaleCell(size, float(np.mean([r.mean_gen_time_s for r in record.repeats])), done, "ok"))
+    return ScaleResult(kind, dataclasses.asdict(base), _metadata(), cells)
+
+
+def _fmt(x: float) -> str:
+    return f"{x:.17g}"
+
+
+def emit(record: RunRecord, fmt: str, out_dir) -> list:
+    """Write a RunRecord as per-repeat CSVs or a single JSON mirror (harness.py:368-395)."""
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    written = []
+    if fmt == "csv":
+        for rep in record.repeats:
+            path = out / f"run_rep{rep.repeat}.csv"
+            with open(path, "w") as fh:
+                for key in ("algorithm", "problem", "seed"):
+                    fh.write(f"# {key}={record.config[key]}\n")
+                fh.write(f"# library={record.metadata['library']}\n")
+                fh.write(f"# repeat={rep.repeat}\n")
+                fh.write(",".join(CSV_COLUMNS) + "\n")
+                for row in rep.rows:
+                    fh.write(f"{row.generation},{_fmt(row.time_s)},{_fmt(row.igd)},{_fmt(row.hv)}\n")
+            written.append(path)
+    elif fmt == "json":
+        path = out / "run.json"
+        with open(path, "w") as fh:
+            json.dump(dataclasses.asdict(record), fh, indent=2)
+        written.append(path)
+    else:
+        raise ConfigError(f"unknown emit format {fmt!r}")
+    return written
+
+
+def emit_scale(result: ScaleResult, out_dir) -> list:
+    """scale.csv plus a JSON mirror (harness.py:398-413)."""
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    csv_path = out / "scale.csv"
+    with open(csv_path, "w") as fh:
+        fh.write(f"# kind={result.kind}\n")
+        fh.write(f"# algorithm={result.config['algorithm']}\n")
+        fh.write(f"# library={result.metadata['library']}\n")
+        fh.write("size,mean_gen_time_s,generations,status\n")
+        for cell in result.cells:
+            fh.write(f"{cell.size},{_fmt(cell.mean_gen_time_s)},{cell.generations_done},{cell.status}\n")
+    json_path = out / "scale.json"
+    with open(json_path, "w") as fh:
+        json.dump(dataclasses.asdict(result), fh, indent=2)
+    return [csv_path, json_path]
+
+
+def parse_run_csv(path) -> tuple:
+    """Read back an emitted per-repeat CSV: (metadata, data rows) (harness.py:416-431)."""
+    meta, rows = {}, []
+    with open(path) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line:
+                continue
+            if line.startswith("#"):
+                key, _, value = line[1:].strip().partition("=")
+                meta[key] = value
+                continue
+            if line.startswith("generation"):
+                continue
+            g, t, gi, gh = line.split(",")
+            rows.append((int(g), float(t), float(gi), float(gh)))
+    return meta, rows

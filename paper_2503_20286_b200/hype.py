@@ -192,6 +192,35 @@ def environmental_selection(X, F, v_ref, n: int, s: int, rng):
     return (Xn.cpu().numpy(), Fn.cpu().numpy()) if is_np else (Xn, Fn)
 
 
-def exact_hype_fitness_oracle(*args, **kwargs):
-    """The reference's cell-decomposition oracle is a CPU test helper (hype.py:88-126)."""
-    raise NotImplementedError("test-only oracle; see oracle/hype.py")
+def exact_hype_fitness_oracle(F, v_ref, k: int, moments: bool = False):
+    """Exact shared-contribution fitness by cell decomposition (hype.py:88-126; n1 <= 8, m <= 3):
+    the grid of point and box coordinates makes dominance constant on every cell, so the fitness
+    integral is a finite sum.  Host code (a test oracle for the Monte-Carlo estimate)."""
+    import itertools
+
+    F = np.asarray(F.cpu().numpy() if hasattr(F, "cpu") else F, dtype=np.float64)
+    v_ref = np.asarray(v_ref, dtype=np.float64)
+    n1, m = F.shape
+    if n1 > 8 or m > 3:
+        raise ValueError("oracle is limited to n1 <= 8, m <= 3")
+    f_l = F.min(axis=0)
+    if np.any(v_ref - f_l <= 0):
+        zero = np.zeros(n1)
+        return (zero, zero.copy()) if moments else zero
+    alpha = shared_alpha(n1, k)
+    axes = []
+    for a in range(m):
+        vals = np.unique(np.concatenate([[f_l[a]], F[:, a], [v_ref[a]]]))
+        axes.append(vals[(vals >= f_l[a]) & (vals <= v_ref[a])])
+    fitness = np.zeros(n1)
+    second = np.zeros(n1)
+    for cell in itertools.product(*(range(len(ax) - 1) for ax in axes)):
+        lo = np.array([axes[a][cell[a]] for a in range(m)])
+        hi = np.array([axes[a][cell[a] + 1] for a in range(m)])
+        vol = np.prod(hi - lo)
+        dom = np.all(F <= lo, axis=1)
+        c = int(dom.sum())
+        if c >= 1:
+            fitness[dom] += vol * alpha[c - 1]
+            second[dom] += vol * alpha[c - 1] ** 2
+    return (fitness, second) if moments else fitness

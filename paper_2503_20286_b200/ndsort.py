@@ -110,5 +110,39 @@ def dominance_matrix(F, block: int = 2048):
 
 
 def ndsort_oracle(F, n: int) -> RankResult:
-    """The reference's sequential oracle is a CPU test helper; not provided on the GPU path."""
-    raise NotImplementedError("use oracle.ndsort.rank_loop (tests only)")
+    """Sequential domination-count sorting (ndsort.py:74-106): the host oracle the batched sort
+    must equal.  Same algorithm and front order as the reference (pairwise counts, then fronts
+    peeled in list order); O(N^2) host work, meant for small N."""
+    A = np.asarray(F.cpu().numpy() if hasattr(F, "cpu") else F, dtype=np.float64)
+    if A.ndim != 2:
+        raise ValueError("objective matrix must be 2-D")
+    N, _ = A.shape
+    dominated_by = np.zeros(N, dtype=np.int64)
+    dominates = []
+    for i in range(N):
+        le_ij = (A[i] <= A).all(axis=1)
+        lt_ij = (A[i] < A).any(axis=1)
+        le_ji = (A <= A[i]).all(axis=1)
+        lt_ji = (A < A[i]).any(axis=1)
+        d_ij = le_ij & lt_ij
+        d_ij[i] = False
+        d_ji = le_ji & lt_ji
+        d_ji[i] = False
+        dominates.append(np.flatnonzero(d_ij))
+        dominated_by[i] = int((d_ji & ~d_ij).sum())
+    r = np.zeros(N, dtype=np.int64)
+    front = [i for i in range(N) if dominated_by[i] == 0]
+    k = 0
+    while front:
+        nxt = []
+        for i in front:
+            r[i] = k
+            for j in dominates[i]:
+                dominated_by[j] -= 1
+                if dominated_by[j] == 0:
+                    nxt.append(int(j))
+        front = nxt
+        k += 1
+    if not 1 <= n <= N:
+        raise ValueError(f"population size {n} out of range [1, {N}]")
+    return RankResult(r, int(np.sort(r)[n - 1]))

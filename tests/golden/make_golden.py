@@ -333,6 +333,54 @@ def gen_moead():
     np.savez_compressed(OUT / "moead.npz", **out)
 
 
+def gen_hype_c():
+    """HypE at BASELINE config C: DTLZ2 m=3, merged N = 20k, n = 10k, s = 100k samples
+    (hype.py:54-163 at the workload size; rank_assign, auto reference, hv_estimate, lexsort)."""
+    seed = 77
+    r = np.random.default_rng(900)
+    spec = problems.make_problem("dtlz2", m=3)
+    N, n, s = 20000, 10000, 100000
+    F = problems.evaluate(spec, r.random((N, spec.d)))
+    res = ndsort.rank_assign(F, n)
+    k = int((res.r <= res.l).sum()) - n
+    ref = hype.auto_reference(F)
+    v_hv = hype.hv_estimate(F, hype.HvEstimateParams(ref, k, s),
+                            np.random.Generator(np.random.Philox(np.random.SeedSequence(seed))))
+    d = np.where(res.r <= res.l, v_hv, -np.finfo(float).max)
+    keep = np.lexsort((np.arange(N), -d, res.r))[:n]
+    np.savez_compressed(OUT / "hype_c.npz", F=F, n=np.array(n), s=np.array(s), seed=np.array(seed), r=res.r.astype(np.int32),
+                        l=np.array(res.l), k=np.array(k), v_ref=ref, v_hv=v_hv, keep=keep.astype(np.int32))
+
+
+def gen_moead_b():
+    """MOEA/D at BASELINE config B: DTLZ2 m=3 d=12, das_dennis(3, 139) -> n = 9870, T = 20,
+    PBI theta = 5; one recorded step after one warm-up step (moead.py:70-158)."""
+    spec = problems.make_problem("dtlz2", m=3, d=12)
+    ds = directions.das_dennis(3, 139)
+    table = directions.neighbors(ds, 20)
+    r = np.random.default_rng(901)
+    X = r.random((ds.count, spec.d))
+    F1 = problems.evaluate(spec, X)
+    st = moead.init_state(X, F1, ds.W, table)
+    params = variation.VariationParams(lower=spec.lower, upper=spec.upper)
+    gen = np.random.Generator(np.random.Philox(np.random.SeedSequence(42)))
+    st = moead.step(st, gen, params, lambda A: problems.evaluate(spec, A))
+    state_before = gen.bit_generator.state
+    rec = RecordingRng(gen)
+    O, F2 = moead.moead_offspring(st, rec, params, lambda A: problems.evaluate(spec, A))
+    upd, z_min = moead.compare_update(st, F2)
+    Xn, Fn = moead.elite_select(st, O, F2, upd, z_min)
+    ints = [v for kind, v in rec.log if kind == "integers"]
+    n, T = ds.count, 20
+    improves = (upd.I_new[np.repeat(np.arange(n), T), st.I_nb.ravel()] == -1).reshape(n, T)
+    np.savez_compressed(OUT / "moead_b.npz", X=st.X, F1=st.F1, z=st.z, I_nb=st.I_nb.astype(np.int16),
+                        O=O, F2=F2, z_min=z_min, Xn=Xn, Fn=Fn, pick1=np.asarray(ints[0]).astype(np.int8),
+                        pick2=np.asarray(ints[1]).astype(np.int8), improves=improves,
+                        counter=state_before["state"]["counter"], key=state_before["state"]["key"],
+                        buffer=state_before["buffer"], buffer_pos=np.array(state_before["buffer_pos"]),
+                        has_uint32=np.array(state_before["has_uint32"]), uinteger=np.array(state_before["uinteger"]))
+
+
 def gen_neighbors():
     out = {}
     for i, (m, H, T) in enumerate(((3, 12, 10), (3, 30, 20), (2, 99, 7), (4, 6, 15))):
@@ -355,10 +403,128 @@ def gen_config_a():
                         final_igd=np.array(rec.repeats[0].final_igd))
 
 
+def gen_config_a_traj():
+    """Config A trajectory, every generation (harness.py:206-248, seed 0, 100 gens): the merged
+    objectives handed to environmental_selection, the shuffle it drew and the objectives it kept,
+    so each generation's selection can be replayed bit for bit on the reference's own inputs."""
+    cfg = RunConfig(algorithm="nsga3", problem="dtlz1", objectives=3, dim=12, pop_size=100, seed=0)
+    spec, R, n = _resolve(cfg)
+    st = _Stepper(cfg, spec, R, n)
+    gen = RngStream(0).split(0).generator()
+    X, F = st.init(gen)
+    Fms, perms, Fsel = [], [], []
+    real = nsga3.environmental_selection
+
+    def spy(Xm, Fm, R_, n_, rng):
+        rec = RecordingRng(rng)
+        Xs, Fs = real(Xm, Fm, R_, n_, rec)
+        Fms.append(Fm.copy())
+        perms.append(np.asarray([v for kind, v in rec.log if kind == "permutation"][0]))
+        Fsel.append(Fs.copy())
+        return Xs, Fs
+
+    nsga3.environmental_selection = spy
+    try:
+        state = (X, F)
+        for g in range(1, 101):
+            state, _ = st.step(state, g, gen)
+    finally:
+        nsga3.environmental_selection = real
+    np.savez_compressed(OUT / "config_a_traj.npz", Fm=np.stack(Fms), perm=np.stack(perms).astype(np.int16),
+                        Fsel=np.stack(Fsel), W=R.W, n=np.array(n))
+
+
+def gen_indicators():
+    """indicators.py:19-100 values from the reference: igd, exact hv (m = 2, 3), Monte-Carlo hv
+    (m = 4, default seeded rng), eu (both readings), on DTLZ fronts and random clouds."""
+    from temo import indicators
+
+    out = {}
+    r = np.random.default_rng(950)
+    cases = []
+    for k, (name, m, n) in enumerate((("dtlz2", 3, 120), ("dtlz1", 3, 300), ("dtlz2", 2, 90), ("dtlz2", 4, 60),
+                                      ("dtlz1", 2, 200), ("dtlz2", 3, 1000))):
+        spec = problems.make_problem(name, m=m)
+        F = problems.evaluate(spec, r.random((n, spec.d)))
+        if k == 4:
+            F[:20] = F[20:40]  # duplicate rows
+            F[40:50, 0] = F[50:60, 0]  # shared x coordinates
+        front = problems.true_front(spec, 200 if m <= 3 else 100)
+        ref = 1.1 * front.max(axis=0)
+        ref[ref <= 0] = 1e-6
+        W = directions.das_dennis(m, 5 if m <= 3 else 3)
+        c = dict(F=F, front=front, ref=ref, W=W.W, igd=indicators.igd(F, front),
+                 hv=indicators.hv_indicator(F, ref), eu=indicators.eu(F, W), eu_lit=indicators.eu(F, W, literal=True),
+                 eu_max=indicators.eu(F, W, maximize=True))
+        cases.append(c)
+    for i, c in enumerate(cases):
+        for key, v in c.items():
+            out[f"c{i}_{key}"] = np.asarray(v)
+    out["count"] = np.array(len(cases))
+    np.savez_compressed(OUT / "indicators.npz", **out)
+
+
+def gen_rvea():
+    """rvea.apd_select (rvea.py:33-68): SPEC acceptance #5 shapes (n <= 32, r <= 16, t = 0 and
+    theta = 0 cases) plus DTLZ-sized instances; winners as row indices."""
+    from temo import rvea
+
+    out = {}
+    r = np.random.default_rng(960)
+    cases = []
+    for k in range(80):
+        m = int(r.integers(2, 5))
+        H = int(r.integers(1, 5))
+        V = directions.das_dennis(m, H)
+        n = int(r.integers(1, 33))
+        F = r.random((n, m))
+        if k % 5 == 0:  # rows collinear with a direction (theta = 0)
+            j = int(r.integers(0, V.count))
+            F[: max(n // 3, 1)] = V.W[j] * r.random((max(n // 3, 1), 1)) * 2 + F.min(axis=0)
+        t_max = int(r.integers(1, 100))
+        t = 0 if k % 7 == 0 else int(r.integers(0, t_max + 1))
+        alpha = float(r.choice([1.0, 2.0, 3.5]))
+        X = np.arange(n, dtype=float)[:, None]
+        Xw, Fw = rvea.apd_select(X, F, V, rvea.ApdParams(alpha, t, t_max))
+        cases.append(dict(F=F, W=V.W, t=t, t_max=t_max, alpha=alpha, keep=Xw[:, 0].astype(np.int64)))
+    for k, (name, m, H, n) in enumerate((("dtlz2", 3, 12, 182), ("dtlz1", 3, 23, 600), ("dtlz2", 5, 4, 140))):
+        spec = problems.make_problem(name, m=m)
+        V = directions.das_dennis(m, H)
+        F = problems.evaluate(spec, r.random((n, spec.d)))
+        X = np.arange(n, dtype=float)[:, None]
+        Xw, Fw = rvea.apd_select(X, F, V, rvea.ApdParams(2.0, 37, 100))
+        cases.append(dict(F=F, W=V.W, t=37, t_max=100, alpha=2.0, keep=Xw[:, 0].astype(np.int64)))
+    for i, c in enumerate(cases):
+        for key, v in c.items():
+            out[f"c{i}_{key}"] = np.asarray(v)
+    out["count"] = np.array(len(cases))
+    np.savez_compressed(OUT / "rvea.npz", **out)
+
+
+def gen_exact_hype():
+    """hype.exact_hype_fitness_oracle (hype.py:88-126) on small instances (n1 <= 8, m <= 3)."""
+    out = {}
+    r = np.random.default_rng(970)
+    cases = []
+    for k in range(12):
+        n1, m = int(r.integers(2, 9)), int(r.integers(2, 4))
+        F = np.round(r.random((n1, m)), 2)
+        ref = F.max(axis=0) + 0.1
+        kk = int(r.integers(1, n1 + 1))
+        fit, sec = hype.exact_hype_fitness_oracle(F, ref, kk, moments=True)
+        cases.append(dict(F=F, ref=ref, k=kk, fit=fit, sec=sec))
+    for i, c in enumerate(cases):
+        for key, v in c.items():
+            out[f"c{i}_{key}"] = np.asarray(v)
+    out["count"] = np.array(len(cases))
+    np.savez_compressed(OUT / "exact_hype.npz", **out)
+
+
 if __name__ == "__main__":
     wanted = set(sys.argv[1:])  # e.g. "gen_linalg": regenerate only those sets
     for fn in (gen_ndsort, gen_nsga3, gen_linalg, gen_associate, gen_hype, gen_variation, gen_problems,
-               gen_moead, gen_neighbors, gen_config_a):
+               gen_moead, gen_neighbors, gen_config_a, gen_hype_c, gen_moead_b, gen_config_a_traj,
+               gen_indicators, gen_rvea, gen_exact_hype):
         if wanted and fn.__name__ not in wanted:
             continue
         fn()

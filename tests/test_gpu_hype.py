@@ -88,3 +88,27 @@ def test_auto_reference(cuda):
 
     F = np.random.default_rng(1).random((300, 4)) * 5 - 1
     assert np.array_equal(auto_reference(F), ohype.auto_reference(F))
+
+
+def test_config_c_golden_bit_exact(cuda):
+    """BASELINE config C at full size (merged N = 20k, n = 10k, s = 100k samples): ranks, l,
+    the HV contributions and the survivor order equal the reference's bits (hype.py:54-163;
+    golden from the reference itself, OPENBLAS_NUM_THREADS=1)."""
+    import torch
+
+    from paper_2503_20286_b200.hype import HypeSelector
+
+    z = dict(load_golden("hype_c"))
+    F = z["F"]
+    N, m = F.shape
+    sel = HypeSelector(N, m, int(z["n"]), int(z["s"]))
+    g = gen(int(z["seed"]))
+    keep = sel.select(torch.from_numpy(F).cuda(), g).cpu().numpy()
+    sel.check()
+    assert int(sel.l.item()) == int(z["l"])
+    r = sel.rank.cpu().numpy()
+    live = z["r"] <= int(z["l"])
+    assert np.array_equal(r[live], z["r"][live])
+    assert sel.info_host.numpy()[1] == int(z["k"])
+    assert np.array_equal(sel.v_hv.cpu().numpy(), z["v_hv"])
+    assert np.array_equal(keep, z["keep"])

@@ -161,3 +161,38 @@ def test_z_monotone_and_tch_runs(cuda):
             assert np.all(z <= prev + 1e-15)
             prev = z
         torch.cuda.synchronize()
+
+
+def test_config_b_golden(cuda):
+    """BASELINE config B at full size: DTLZ2 m=3 d=12, n = 9870 directions (H = 139), T = 20, with
+    19 % exact T-th neighbour ties.  Offspring within pow ulps; z_min, improves and the elite
+    selection on the reference's offspring bit-exact (moead.py:70-158)."""
+    import torch
+
+    from paper_2503_20286_b200.directions import DirectionSet, NeighborTable, das_dennis
+    from paper_2503_20286_b200.moead import MoeadEngine, MoeadState
+    from paper_2503_20286_b200.problems import make_problem
+    from paper_2503_20286_b200.variation import VariationParams
+
+    z = dict(load_golden("moead_b"))
+    spec = make_problem("dtlz2", m=3, d=12)
+    R = das_dennis(3, 139)
+    I_nb = z["I_nb"].astype(np.int64)
+    eng = MoeadEngine(spec, R, NeighborTable(I_nb), VariationParams(lower=spec.lower, upper=spec.upper), 5.0, "pbi")
+    dev = eng.dev
+    st = MoeadState(torch.from_numpy(z["X"]).to(dev), torch.from_numpy(z["F1"]).to(dev),
+                    torch.from_numpy(z["z"]).to(dev), eng.W, eng.I_nb, 5.0)
+    g = np.random.Generator(np.random.Philox())
+    s = g.bit_generator.state
+    s["state"]["counter"], s["state"]["key"] = z["counter"], z["key"]
+    s["buffer"], s["buffer_pos"] = z["buffer"], int(z["buffer_pos"])
+    s["has_uint32"], s["uinteger"] = int(z["has_uint32"]), int(z["uinteger"])
+    g.bit_generator.state = s
+    eng.step(st, g)
+    assert np.allclose(eng.O.cpu().numpy(), z["O"], rtol=1e-13, atol=1e-14)
+    assert np.allclose(eng.F2.cpu().numpy(), z["F2"], rtol=1e-10, atol=1e-12)
+    nxt = eng.select(st, torch.from_numpy(z["O"]).to(dev), torch.from_numpy(z["F2"]).to(dev))
+    assert np.array_equal(eng.zmin.cpu().numpy(), z["z_min"])
+    assert np.array_equal(eng.improves.cpu().numpy().astype(bool), z["improves"])
+    assert np.array_equal(nxt.X.cpu().numpy(), z["Xn"])
+    assert np.array_equal(nxt.F1.cpu().numpy(), z["Fn"])

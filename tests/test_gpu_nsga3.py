@@ -284,3 +284,48 @@ def test_intercept_solve_lapack_bits_all_m(cuda):
     bad = [int(ms[i]) for i in range(len(ms)) if not np.array_equal(got[z["y_off"][i]:z["y_off"][i + 1]],
                                                                      z["y"][z["y_off"][i]:z["y_off"][i + 1]])]
     assert not bad, f"mismatches at m = {sorted(set(bad))}"
+
+
+@pytest.mark.parametrize("N,kind", [(20000, "lsmop1"), (40000, "lsmop1"), (20000, "dtlz2-ties")])
+def test_selection_vs_oracle_workload_scale(cuda, N, kind):
+    """Full NSGA-III selection (nsga3.py:186-218) at workload sizes (merged N = 20k / 40k, i.e.
+    pop 10k / 20k of config D) on LSMOP1 objectives and on tie-heavy DTLZ2 objectives: ranks, l,
+    association (pi, dist), promotions and survivors bit-exact against the CPU oracle
+    (reference-pinned restatement; ranks by the O(N) memory longest-chain oracle)."""
+    import torch
+
+    from oracle import ndsort as ond
+    from oracle import problems as oprob
+    from paper_2503_20286_b200.directions import das_dennis, largest_h_for
+    from paper_2503_20286_b200.nsga3 import Nsga3Selector
+
+    rng = np.random.default_rng(N + len(kind))
+    m, n = 3, N // 2
+    if kind == "lsmop1":
+        D = oprob.lsmop_dimension(m, 1000)
+        lo, hi = oprob.lsmop_bounds(m, D)
+        X = lo + rng.random((N, D)) * (hi - lo)
+        X[:, 2:] = X[:, :1] * 10.0 / (1.0 + np.arange(m, D + 1) / D) + rng.normal(0, 0.3, (N, D - 2))  # near the front
+        F = oprob.evaluate_lsmop1(np.clip(X, lo, hi), m)
+    else:
+        F = oprob.evaluate_dtlz("dtlz2", rng.random((N, 12)), m)
+        F[: N // 3] = np.round(F[: N // 3], 2)  # exact ties between rows and in every column
+    R = das_dennis(m, largest_h_for(n, m))
+    perm = rng.permutation(N)
+    Fs = F[perm]
+    sel = Nsga3Selector(N, m, R, n, record=True)
+    keep = sel.select_shuffled(torch.from_numpy(Fs).cuda()).cpu().numpy()
+    sel.check()
+    want = onsga3.select_shuffled(Fs, R.W, n, rank_fn=ond.rank_fast)
+    l = int(sel.l.item())
+    assert l == want["l"]
+    live = want["r"] <= l
+    # sel.rank holds the ranks after niche promotion / repair (nsga3.py:212-213)
+    assert np.array_equal(sel.rank.cpu().numpy()[live], want["rank"][live])
+    assert np.array_equal(sel.ideal.cpu().numpy(), want["ideal"])
+    assert np.array_equal(sel.icpt.cpu().numpy(), want["intercepts"])
+    assert np.array_equal(sel.pi.cpu().numpy()[live], want["pi"][live])
+    assert np.array_equal(sel.dist.cpu().numpy()[live], want["dist"][live])
+    k = int(sel.counts[0].item())
+    assert np.array_equal(sel.promoted[:k].cpu().numpy(), want["promoted"])
+    assert np.array_equal(keep, want["keep"])

@@ -134,3 +134,39 @@ def test_host_permutation_bit_exact_with_numpy():
                 assert np.array_equal(a.permutation(n), R.permutation(b, n)), (seed, pre, n)
                 assert same(a.bit_generator.state, b.bit_generator.state), (seed, pre, n)
                 assert np.array_equal(a.random(3), b.random(3))
+
+
+def test_ndsort_oracle_host_matches_reference_golden():
+    """ndsort_oracle (ndsort.py:74-106) is provided as a host oracle: same ranks as the reference."""
+    from conftest import load_golden, unpack
+    from paper_2503_20286_b200.ndsort import ndsort_oracle
+
+    z = dict(load_golden("ndsort"))
+    for i in range(0, len(z["N"]), 5):
+        N, m, n = int(z["N"][i]), int(z["m"][i]), int(z["n"][i])
+        if N > 400:
+            continue
+        F = unpack(z["F"], z["F_off"], i).reshape(N, m)
+        res = ndsort_oracle(F, n)
+        assert np.array_equal(res.r, unpack(z["r"], z["r_off"], i)) and res.l == int(z["l"][i])
+
+
+def test_run_config_fields_match_reference():
+    import dataclasses
+
+    from paper_2503_20286_b200.harness import ConfigError, RunConfig
+
+    names = {f.name for f in dataclasses.fields(RunConfig)}
+    for f in ("algorithm", "problem", "objectives", "dim", "pop_size", "generations", "seed", "repeats",
+              "eta_c", "eta_m", "pm", "theta", "neighborhood", "divisions", "alpha", "hv_samples", "hv_ref",
+              "indicators", "indicator_every", "ref_front_size", "time_selection_only", "out"):
+        assert f in names
+    with pytest.raises(ConfigError):
+        RunConfig(indicators=("nope",)).validate()
+    with pytest.raises(ConfigError):
+        RunConfig(ref_front_size=2).validate()
+    with pytest.raises(ConfigError):
+        RunConfig(hv_ref="1,2").validate()
+    with pytest.raises(ConfigError):
+        RunConfig(algorithm="nsga3-seq").validate()
+    RunConfig(algorithm="rvea").validate()
