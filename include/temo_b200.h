@@ -258,6 +258,14 @@ int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const
                       const int64_t *i1, const int64_t *i2, int64_t h, const temo_philox_state *st,
                       uint64_t off, double *O, double *FO, const int64_t *src_map,
                       const int64_t *dst_rows, void *ws, size_t ws_bytes, temo_stream_t stream);
+/* Row-sharded form: only the pairs [q0, q1) of the h pairs, with exactly the
+ * draws and output rows the full call gives them (Philox elements are indexed by the global
+ * pair), so G ranks covering [0, h) together produce the full result bit for bit. */
+int temo_offspring_ws_range(const temo_problem *prob, const temo_variation *var, const double *X,
+                            const int64_t *i1, const int64_t *i2, int64_t h, int64_t q0, int64_t q1,
+                            const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                            const int64_t *src_map, const int64_t *dst_rows, void *ws, size_t ws_bytes,
+                            temo_stream_t stream);
 
 /* Row-pool bookkeeping after a selection (replaces the survivor row copy X[perm][keep] of
  * nsga3.py:218 / hype.py:163): phys (N) maps logical merged rows to pool rows; the n
@@ -324,6 +332,24 @@ int temo_hype_select(const double *F, int64_t N, int m, int64_t n, int64_t s, co
                      const int32_t *rank, const int32_t *l, const temo_philox_state *st,
                      uint64_t off, const double *U, int32_t *keep, double *v_hv, int32_t *info,
                      void *ws, size_t ws_bytes, temo_stream_t stream);
+
+/* temo_hype_select in three phases (same workspace, same results) so the Monte-Carlo work
+ * can be sharded over GPUs by exchange column: the s samples fall in 65,536-sample
+ * blocks, each giving its 2,048-sample sub-blocks plus one b % 4 tail as columns
+ * (temo_hype_columns(s) in total).  begin: k, alpha, box.  columns: the N-row partial sums
+ * of columns [c_lo, c_hi) into Tseg (column-major, N per column; NULL = the workspace's own
+ * full buffer).  end: combine all columns of Tg (N x temo_hype_columns(s), column-major; NULL =
+ * the workspace's buffer) in the reference's summation order, then the lexsort -> keep.
+ * Ranks that each fill a column range and all-gather Tg reproduce the single-GPU bits. */
+int64_t temo_hype_columns(int64_t s);
+int temo_hype_select_begin(const double *F, int64_t N, int m, int64_t n, int64_t s, const double *v_ref,
+                           const int32_t *rank, const int32_t *l, void *ws, size_t ws_bytes, temo_stream_t stream);
+int temo_hype_select_columns(const double *F, int64_t N, int m, int64_t s, int64_t c_lo, int64_t c_hi,
+                             const temo_philox_state *st, uint64_t off, const double *U, double *Tseg, void *ws,
+                             size_t ws_bytes, temo_stream_t stream);
+int temo_hype_select_end(const double *F, int64_t N, int m, int64_t n, int64_t s, const int32_t *rank,
+                         const int32_t *l, const double *Tg, int32_t *keep, double *v_hv, int32_t *info, void *ws,
+                         size_t ws_bytes, temo_stream_t stream);
 
 /* The normalize kernel's np.linalg.solve(E, ones) (nsga3.py:86; OpenBLAS getf2 / blocked
  * getrf order, bit-exact for m <= 16) on `count` row-major matrices E + E_off[i] of size

@@ -76,6 +76,8 @@ SIGNATURES = {
     "temo_offspring": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _U64, _P, _P, _P]),
     "temo_offspring_ws_bytes": (_SZ, [_I64, _I64]),
     "temo_offspring_ws": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _U64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "temo_offspring_ws_range": (_I32, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _U64, _P, _P, _P, _P, _P, _SZ,
+                                       _P]),
     "temo_pool_update_ws_bytes": (_SZ, [_I64]),
     "temo_pool_update": (_I32, [_P, _P, _P, _I64, _I64, _P, _P, _P, _SZ, _P]),
     "temo_init_population": (_I32, [_P, _U64, _I64, _I64, _P, _P, _P, _P]),
@@ -89,6 +91,10 @@ SIGNATURES = {
     "temo_hv_estimate_ws_bytes": (_SZ, [_I64, _I32, _I64]),
     "temo_hv_estimate": (_I32, [_P, _I64, _I32, _P, _I64, _I64, _P, _U64, _P, _P, _P, _P, _SZ, _P]),
     "temo_hype_select_ws_bytes": (_SZ, [_I64, _I32, _I64]),
+    "temo_hype_columns": (_I64, [_I64]),
+    "temo_hype_select_begin": (_I32, [_P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
+    "temo_hype_select_columns": (_I32, [_P, _I64, _I32, _I64, _I64, _I64, _P, _U64, _P, _P, _P, _SZ, _P]),
+    "temo_hype_select_end": (_I32, [_P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "temo_hype_select": (_I32, [_P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _U64, _P, _P, _P, _P, _P,
                                 _SZ, _P]),
     "temo_probe_philox_rate": (_D, [_I32, _I32, _P, _P]),

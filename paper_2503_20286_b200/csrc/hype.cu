@@ -202,7 +202,8 @@ __global__ void k_hv_weights(const int32_t *__restrict__ cnt, int64_t b, const d
 
 // ---------------------------------------------------------------- pass 2 (App. A7 order)
 // One CTA per (sub-block g, 64 points); 4 threads per point = the 4 dgemv lanes.
-// T[i * nsub + g] = (s0 + s2) + (s1 + s3)   (4-lane rows)   or   s0 + s1   (2-lane rows)
+// T[g * n1 + i] = (s0 + s2) + (s1 + s3)   (4-lane rows)   or   s0 + s1   (2-lane rows);
+// column-major so a rank's contiguous range of sub-block columns is one exchange segment.
 __global__ void __launch_bounds__(256) k_hv_partial(const uint32_t *__restrict__ bits, int64_t Wb,
                                                     int64_t n1, int64_t b4, int nsub,
                                                     const double *__restrict__ w,
@@ -242,27 +243,44 @@ __global__ void __launch_bounds__(256) k_hv_partial(const uint32_t *__restrict__
     const double a1 = __shfl_down_sync(~0u, acc, 1);
     const double a2 = __shfl_down_sync(~0u, acc, 2);
     const double a3 = __shfl_down_sync(~0u, acc, 3);
-    if (ln == 0 && i < n1) T[i * nsub + g] = two ? acc + a1 : (acc + a2) + (a1 + a3);
+    if (ln == 0 && i < n1) T[(int64_t)g * n1 + i] = two ? acc + a1 : (acc + a2) + (a1 + a3);
 }
 
-// y per point: sequential over sub-blocks, then the b % 4 tail grouped; contrib += y
-__global__ void k_hv_combine(const double *__restrict__ T, int nsub, const uint32_t *__restrict__ bits,
-                             int64_t Wb, int64_t n1, int64_t b4, int64_t b, const double *__restrict__ w,
-                             const int32_t *__restrict__ ok, double *__restrict__ contrib) {
+// the b % 4 tail of a sample block (relative samples [t0, t0 + tlen) of the bitmap): the
+// grouped sum ((p0 + p1) + p2) of the tail products (App. A7) -> one exchange column
+__global__ void k_hv_tail(const uint32_t *__restrict__ bits, int64_t Wb, int64_t n1, int64_t t0, int64_t tlen,
+                          const double *__restrict__ w, const int32_t *__restrict__ ok, double *__restrict__ col) {
     if (!*ok) return;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n1) return;
-    double y = 0.0;
-    for (int g = 0; g < nsub; ++g) y = y + T[i * nsub + g];
-    if (b4 < b) {
-        double tail = 0.0;
-        for (int64_t e = b4; e < b; ++e) {
-            const double p = ((bits[i * Wb + e / 32] >> (e & 31)) & 1u) ? w[e] : 0.0;
-            tail = e == b4 ? p : tail + p;
-        }
-        y = y + tail;
+    double tail = 0.0;
+    for (int64_t e = t0; e < t0 + tlen; ++e) {
+        const double p = ((bits[i * Wb + e / 32] >> (e & 31)) & 1u) ? w[e] : 0.0;
+        tail = e == t0 ? p : tail + p;
     }
-    contrib[i] = contrib[i] + y;
+    col[i] = tail;
+}
+
+// per point over every sample block in order: y = sum of its sub-block columns (sequential),
+// + the tail column if the block has a b % 4 tail; contrib = contrib + y (hype.py:83)
+__global__ void k_hv_combine(const double *__restrict__ Tg, int64_t n1, int64_t s, const int32_t *__restrict__ ok,
+                             double *__restrict__ contrib) {
+    if (!*ok) return;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n1) return;
+    double c = 0.0;
+    int64_t col = 0;
+    for (int64_t e0 = 0; e0 < s; e0 += SAMPLE_BLOCK) {
+        const int64_t b = s - e0 < SAMPLE_BLOCK ? s - e0 : SAMPLE_BLOCK;
+        const int64_t b4 = b - b % 4;
+        const int64_t nsub = (b4 + SUB - 1) / SUB;
+        double y = 0.0;
+        for (int64_t g = 0; g < nsub; ++g) y = y + Tg[(col + g) * n1 + i];
+        if (b4 < b) y = y + Tg[(col + nsub) * n1 + i];
+        c = c + y;
+        col += nsub + 1;
+    }
+    contrib[i] = c;
 }
 
 __global__ void k_hv_final(double *__restrict__ contrib, int64_t n1, const double *__restrict__ P,
@@ -317,6 +335,16 @@ struct HvPlan {
     size_t total;
 };
 
+// exchange columns of s samples: per 65,536-sample block its 2048-sample sub-blocks + one tail column
+static int64_t hv_columns(int64_t s) {
+    int64_t c = 0;
+    for (int64_t e0 = 0; e0 < s; e0 += SAMPLE_BLOCK) {
+        const int64_t b = s - e0 < SAMPLE_BLOCK ? s - e0 : SAMPLE_BLOCK;
+        c += (b - b % 4 + SUB - 1) / SUB + 1;
+    }
+    return c;
+}
+
 static void plan_hv(HvPlan &p, void *base, int64_t n1, int m, int64_t s) {
     p.n1 = n1;
     p.m = m;
@@ -336,54 +364,91 @@ static void plan_hv(HvPlan &p, void *base, int64_t n1, int m, int64_t s) {
     p.w = c.take<double>(b);
     p.cnt = c.take<int32_t>(b);
     p.bits = c.take<uint32_t>((size_t)n1 * p.Wb);
-    p.T = c.take<double>((size_t)n1 * p.nsub_max);
+    p.T = c.take<double>((size_t)n1 * hv_columns(s));
     p.contrib = c.take<double>(n1);
     p.total = c.off;
 }
 
 static inline dim3 gdim(int64_t n, int t = 256) { return dim3((unsigned)((n + t - 1) / t)); }
 
-// hv_estimate body; `ok` must already hold whether to estimate (k >= 1 and box check
-// happens here).  v_hv receives the contributions (zeros when the box is degenerate).
-static int hv_run(HvPlan &p, const double *F, const double *vref_in, const temo_philox_state *st,
-                  uint64_t off, const double *U, double *v_hv, cudaStream_t sm) {
+// hv_estimate, split so a multi-GPU run can shard the samples by exchange column
+// (SURVEY 8e): prepare (box, P, ok) -> columns [c_lo, c_hi) of Tg -> (all-gather) -> combine.
+// `ok` must already hold whether to estimate (k >= 1); the box check happens here.
+static void hv_prepare(HvPlan &p, const double *F, const double *vref_in, cudaStream_t sm) {
+    k_minmax_cols<<<p.m, 256, 0, sm>>>(F, p.n1, p.m, p.mn, p.mx);
+    k_hv_box<<<1, 1, 0, sm>>>(p.mn, p.mx, vref_in, p.m, p.vref, p.span, p.P, p.ok);
+}
+
+static int hv_cols(HvPlan &p, const double *F, const temo_philox_state *st, uint64_t off, const double *U,
+                   int64_t c_lo, int64_t c_hi, double *Tg, cudaStream_t sm) {
     const int64_t n1 = p.n1, s = p.s;
     const int m = p.m;
-    k_minmax_cols<<<m, 256, 0, sm>>>(F, n1, m, p.mn, p.mx);
-    k_hv_box<<<1, 1, 0, sm>>>(p.mn, p.mx, vref_in, m, p.vref, p.span, p.P, p.ok);
-    TEMO_CUDA(cudaMemsetAsync(p.contrib, 0, sizeof(double) * n1, sm));
     const Philox ph = st ? philox_from(*st) : Philox{};
     const int64_t two_lo = (n1 % 4 == 2 || n1 % 4 == 3) ? n1 - n1 % 4 : -1;
     const int64_t two_hi = two_lo >= 0 ? two_lo + 2 : -1;
+    int64_t cb = 0;  // first exchange column of the block
     for (int64_t e0 = 0; e0 < s; e0 += SAMPLE_BLOCK) {
         const int64_t b = s - e0 < SAMPLE_BLOCK ? s - e0 : SAMPLE_BLOCK;
         const int64_t b4 = b - b % 4;
-        const int nsub = (int)((b4 + SUB - 1) / SUB);
-        k_hv_samples<<<gdim((b * m + 3) / 4), 256, 0, sm>>>(ph, off, U, e0, b, m, p.mn, p.span, p.ok, p.S);
-        TEMO_CUDA(cudaMemsetAsync(p.cnt, 0, sizeof(int32_t) * b, sm));
-        stage_begin(S_HV_COUNT, sm);
-        dim3 g1((unsigned)((n1 + HT - 1) / HT), (unsigned)((b + HT - 1) / HT));
-#define HVD(MM) case MM: k_hv_dom<MM><<<g1, HT, 0, sm>>>(F, n1, p.S, b, p.ok, p.Wb, p.bits, p.cnt); break;
-        switch (m) {
-            HVD(1) HVD(2) HVD(3) HVD(4) HVD(5) HVD(6) HVD(7) HVD(8) HVD(9) HVD(10) HVD(11) HVD(12)
-            HVD(13) HVD(14) HVD(15) HVD(16)
-            default: return TEMO_EINVAL;
-        }
+        const int64_t nsub = (b4 + SUB - 1) / SUB;
+        const int64_t lo = c_lo - cb > 0 ? c_lo - cb : 0, hi = c_hi - cb < nsub + 1 ? c_hi - cb : nsub + 1;
+        if (lo < hi) {
+            // this rank's samples of the block: sub-blocks [lo, min(hi, nsub)) then the tail
+            const int64_t e_lo = lo < nsub ? lo * SUB : b4;
+            const int64_t e_hi = hi > nsub ? b : (hi * SUB < b4 ? hi * SUB : b4);
+            const int64_t len = e_hi - e_lo;
+            if (len > 0) {
+                const int64_t Wb = (len + 31) / 32;
+                k_hv_samples<<<gdim((len * m + 3) / 4), 256, 0, sm>>>(ph, off, U, e0 + e_lo, len, m, p.mn, p.span,
+                                                                      p.ok, p.S);
+                TEMO_CUDA(cudaMemsetAsync(p.cnt, 0, sizeof(int32_t) * len, sm));
+                stage_begin(S_HV_COUNT, sm);
+                dim3 g1((unsigned)((n1 + HT - 1) / HT), (unsigned)((len + HT - 1) / HT));
+#define HVD(MM) case MM: k_hv_dom<MM><<<g1, HT, 0, sm>>>(F, n1, p.S, len, p.ok, Wb, p.bits, p.cnt); break;
+                switch (m) {
+                    HVD(1) HVD(2) HVD(3) HVD(4) HVD(5) HVD(6) HVD(7) HVD(8) HVD(9) HVD(10) HVD(11) HVD(12)
+                    HVD(13) HVD(14) HVD(15) HVD(16)
+                    default: return TEMO_EINVAL;
+                }
 #undef HVD
-        stage_end(S_HV_COUNT, sm);
-        k_hv_weights<<<gdim(b), 256, 0, sm>>>(p.cnt, b, p.alpha, p.ok, p.w);
-        stage_begin(S_HV_CONTRIB, sm);
-        if (nsub > 0) {
-            dim3 g2((unsigned)((n1 + 63) / 64), (unsigned)nsub);
-            k_hv_partial<<<g2, 256, 0, sm>>>(p.bits, p.Wb, n1, b4, nsub, p.w, p.ok, two_lo, two_hi, p.T);
+                stage_end(S_HV_COUNT, sm);
+                k_hv_weights<<<gdim(len), 256, 0, sm>>>(p.cnt, len, p.alpha, p.ok, p.w);
+                stage_begin(S_HV_CONTRIB, sm);
+                const int64_t sub_hi = hi < nsub ? hi : nsub;
+                if (lo < sub_hi) {
+                    const int64_t b4r = (b4 < e_hi ? b4 : e_hi) - e_lo;
+                    dim3 g2((unsigned)((n1 + 63) / 64), (unsigned)(sub_hi - lo));
+                    k_hv_partial<<<g2, 256, 0, sm>>>(p.bits, Wb, n1, b4r, (int)(sub_hi - lo), p.w, p.ok, two_lo, two_hi,
+                                                     Tg + (cb + lo - c_lo) * n1);
+                }
+                if (hi > nsub && b4 < b)  // the tail column
+                    k_hv_tail<<<gdim(n1), 256, 0, sm>>>(p.bits, Wb, n1, b4 - e_lo, b - b4, p.w, p.ok,
+                                                        Tg + (cb + nsub - c_lo) * n1);
+                stage_end(S_HV_CONTRIB, sm);
+            }
         }
-        k_hv_combine<<<gdim(n1), 256, 0, sm>>>(p.T, nsub, p.bits, p.Wb, n1, b4, b, p.w, p.ok, p.contrib);
-        stage_end(S_HV_CONTRIB, sm);
+        cb += nsub + 1;
     }
-    k_hv_final<<<gdim(n1), 256, 0, sm>>>(p.contrib, n1, p.P, s, p.ok);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
+static int hv_combine_final(HvPlan &p, const double *Tg, double *v_hv, cudaStream_t sm) {
+    const int64_t n1 = p.n1;
+    TEMO_CUDA(cudaMemsetAsync(p.contrib, 0, sizeof(double) * n1, sm));
+    k_hv_combine<<<gdim(n1), 256, 0, sm>>>(Tg, n1, p.s, p.ok, p.contrib);
+    k_hv_final<<<gdim(n1), 256, 0, sm>>>(p.contrib, n1, p.P, p.s, p.ok);
     TEMO_CUDA(cudaMemcpyAsync(v_hv, p.contrib, sizeof(double) * n1, cudaMemcpyDeviceToDevice, sm));
     TEMO_LAUNCH_CHECK();
     return TEMO_OK;
+}
+
+static int hv_run(HvPlan &p, const double *F, const double *vref_in, const temo_philox_state *st,
+                  uint64_t off, const double *U, double *v_hv, cudaStream_t sm) {
+    hv_prepare(p, F, vref_in, sm);
+    const int rc = hv_cols(p, F, st, off, U, 0, hv_columns(p.s), p.T, sm);
+    if (rc) return rc;
+    return hv_combine_final(p, p.T, v_hv, sm);
 }
 
 struct SelHPlan {
@@ -475,36 +540,66 @@ extern "C" size_t temo_hype_select_ws_bytes(int64_t N, int m, int64_t s) {
     return round_up(a.total, 256) + h.total;
 }
 
-// hype.environmental_selection core (hype.py:153-163) on ranks from temo_rank
-// (SELECT mode).  k >= 1 is decided on the device; `info` (int32[4]) receives
-// {count(r <= l), k, estimated, box_ok}: the host advances its Generator by
-// s*m outputs iff estimated && box_ok.
-extern "C" int temo_hype_select(const double *F, int64_t N, int m, int64_t n, int64_t s,
-                                const double *v_ref, const int32_t *rank, const int32_t *l,
-                                const temo_philox_state *st, uint64_t off, const double *U,
-                                int32_t *keep, double *v_hv, int32_t *info, void *ws, size_t ws_bytes,
-                                temo_stream_t stream) {
-    if (!F || N < 1 || m < 1 || m > 16 || n < 1 || n > N || s < 1 || !rank || !l || !keep || !v_hv)
-        return TEMO_EINVAL;
-    if (!st && !U) return TEMO_EINVAL;
-    cudaStream_t sm = (cudaStream_t)stream;
+// hype.environmental_selection core (hype.py:153-163) on ranks from temo_rank (SELECT mode),
+// in three phases so the Monte-Carlo columns can be sharded over ranks:
+//   begin   : k = count(r <= l) - n (device), alpha, box / P / ok
+//   columns : exchange columns [c_lo, c_hi) of the contribution partials (column-major n1 x C)
+//   end     : combine every column in the reference's order, lexsort (rank, -v_hv, index) -> keep
+// `info` (int32[4]) receives {count(r <= l), k, estimated, box_ok}: the host advances its
+// Generator by s*m outputs iff estimated && box_ok.
+struct HypeWs {
     SelHPlan a;
-    plan_selh(a, nullptr, N);
     HvPlan h;
-    plan_hv(h, nullptr, N, m, s);
-    if (!ws || ws_bytes < round_up(a.total, 256) + h.total) return TEMO_EWORKSPACE;
-    plan_selh(a, ws, N);
-    plan_hv(h, static_cast<char *>(ws) + round_up(a.total, 256), N, m, s);
+};
+
+static int hype_ws(HypeWs &w, void *ws, size_t ws_bytes, int64_t N, int m, int64_t s) {
+    plan_selh(w.a, nullptr, N);
+    plan_hv(w.h, nullptr, N, m, s);
+    if (!ws || ws_bytes < round_up(w.a.total, 256) + w.h.total) return TEMO_EWORKSPACE;
+    plan_selh(w.a, ws, N);
+    plan_hv(w.h, static_cast<char *>(ws) + round_up(w.a.total, 256), N, m, s);
+    return TEMO_OK;
+}
+
+extern "C" int64_t temo_hype_columns(int64_t s) { return s < 1 ? 0 : hv_columns(s); }
+
+extern "C" int temo_hype_select_begin(const double *F, int64_t N, int m, int64_t n, int64_t s, const double *v_ref,
+                                      const int32_t *rank, const int32_t *l, void *ws, size_t ws_bytes,
+                                      temo_stream_t stream) {
+    if (!F || N < 1 || m < 1 || m > 16 || n < 1 || n > N || s < 1 || !rank || !l) return TEMO_EINVAL;
+    HypeWs w;
+    if (int rc = hype_ws(w, ws, ws_bytes, N, m, s)) return rc;
+    cudaStream_t sm = (cudaStream_t)stream;
     stage_begin(S_HYPE_SELECT, sm);
-    TEMO_CUDA(cudaMemsetAsync(a.scal, 0, sizeof(int32_t) * 8, sm));
-    k_hype_k<<<gdim(N), 256, 0, sm>>>(rank, l, N, n, a.scal);
-    // alpha needs k on the host-visible path: compute it on the device from scal
-    k_hype_k_final<<<1, 1, 0, sm>>>(a.scal, n, h.ok);
+    TEMO_CUDA(cudaMemsetAsync(w.a.scal, 0, sizeof(int32_t) * 8, sm));
+    k_hype_k<<<gdim(N), 256, 0, sm>>>(rank, l, N, n, w.a.scal);
+    k_hype_k_final<<<1, 1, 0, sm>>>(w.a.scal, n, w.h.ok);  // estimation only if k >= 1 (hype.py:156)
     stage_end(S_HYPE_SELECT, sm);
-    // estimation (every kernel is a no-op when ok == 0); alpha from the device-side k
-    k_alpha_dev<<<1, 1, 0, sm>>>(N, a.scal, h.alpha);
-    const int rc = hv_run(h, F, v_ref, st, off, U, v_hv, sm);
-    if (rc) return rc;
+    k_alpha_dev<<<1, 1, 0, sm>>>(N, w.a.scal, w.h.alpha);
+    hv_prepare(w.h, F, v_ref, sm);
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
+extern "C" int temo_hype_select_columns(const double *F, int64_t N, int m, int64_t s, int64_t c_lo, int64_t c_hi,
+                                        const temo_philox_state *st, uint64_t off, const double *U, double *Tseg,
+                                        void *ws, size_t ws_bytes, temo_stream_t stream) {
+    if (!F || N < 1 || m < 1 || m > 16 || s < 1 || c_lo < 0 || c_hi < c_lo || c_hi > hv_columns(s)) return TEMO_EINVAL;
+    if (!st && !U) return TEMO_EINVAL;
+    HypeWs w;
+    if (int rc = hype_ws(w, ws, ws_bytes, N, m, s)) return rc;
+    return hv_cols(w.h, F, st, off, U, c_lo, c_hi, Tseg ? Tseg : w.h.T + c_lo * N, (cudaStream_t)stream);
+}
+
+extern "C" int temo_hype_select_end(const double *F, int64_t N, int m, int64_t n, int64_t s, const int32_t *rank,
+                                    const int32_t *l, const double *Tg, int32_t *keep, double *v_hv, int32_t *info,
+                                    void *ws, size_t ws_bytes, temo_stream_t stream) {
+    if (!F || N < 1 || m < 1 || m > 16 || n < 1 || n > N || s < 1 || !rank || !l || !keep || !v_hv) return TEMO_EINVAL;
+    HypeWs w;
+    if (int rc = hype_ws(w, ws, ws_bytes, N, m, s)) return rc;
+    cudaStream_t sm = (cudaStream_t)stream;
+    if (int rc = hv_combine_final(w.h, Tg ? Tg : w.h.T, v_hv, sm)) return rc;
+    SelHPlan &a = w.a;
     stage_begin(S_HYPE_SELECT, sm);
     k_hype_keys<<<gdim(N), 256, 0, sm>>>(rank, l, v_hv, a.scal, N, a.key_a, a.idx_a);
     size_t tb = a.cub_bytes;
@@ -514,9 +609,23 @@ extern "C" int temo_hype_select(const double *F, int64_t N, int m, int64_t n, in
     TEMO_CUDA(cudaMemcpyAsync(keep, a.idx_a, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, sm));
     if (info) {
         TEMO_CUDA(cudaMemcpyAsync(info, a.scal, sizeof(int32_t) * 3, cudaMemcpyDeviceToDevice, sm));
-        TEMO_CUDA(cudaMemcpyAsync(info + 3, h.ok, sizeof(int32_t), cudaMemcpyDeviceToDevice, sm));
+        TEMO_CUDA(cudaMemcpyAsync(info + 3, w.h.ok, sizeof(int32_t), cudaMemcpyDeviceToDevice, sm));
     }
     stage_end(S_HYPE_SELECT, sm);
     TEMO_LAUNCH_CHECK();
     return TEMO_OK;
+}
+
+extern "C" int temo_hype_select(const double *F, int64_t N, int m, int64_t n, int64_t s,
+                                const double *v_ref, const int32_t *rank, const int32_t *l,
+                                const temo_philox_state *st, uint64_t off, const double *U,
+                                int32_t *keep, double *v_hv, int32_t *info, void *ws, size_t ws_bytes,
+                                temo_stream_t stream) {
+    if (!F || N < 1 || m < 1 || m > 16 || n < 1 || n > N || s < 1 || !rank || !l || !keep || !v_hv)
+        return TEMO_EINVAL;
+    if (!st && !U) return TEMO_EINVAL;
+    if (int rc = temo_hype_select_begin(F, N, m, n, s, v_ref, rank, l, ws, ws_bytes, stream)) return rc;
+    if (int rc = temo_hype_select_columns(F, N, m, s, 0, hv_columns(s), st, off, U, nullptr, ws, ws_bytes, stream))
+        return rc;
+    return temo_hype_select_end(F, N, m, n, s, rank, l, nullptr, keep, v_hv, info, ws, ws_bytes, stream);
 }

@@ -967,7 +967,8 @@ constexpr int RW = 8;  // warps per CTA of both phases
 __host__ __device__ inline int64_t quads_per_pair(int64_t d) { return (d + 3) / 4 + 1; }
 
 template <bool SWAP>
-__global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64_t d, VarArgs V, int64_t h, Philox ph,
+__global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64_t d, VarArgs V, int64_t h,
+                                                               int64_t q0, int64_t q1, Philox ph,
                                                                uint64_t off, int single,
                                                                double *__restrict__ beta,
                                                                uint16_t *__restrict__ flags) {
@@ -983,7 +984,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64
     if (V.p_m >= 1.0) pm_thr = INT64_MAX;
     else if (V.p_m >= 0.0) pm_thr = (int64_t)floor(V.p_m * 9007199254740992.0);
     const int64_t QP = quads_per_pair(d);
-    for (int64_t q = (int64_t)blockIdx.x * RW + warp; q < h; q += (int64_t)gridDim.x * RW) {
+    for (int64_t q = q0 + (int64_t)blockIdx.x * RW + warp; q < q1; q += (int64_t)gridDim.x * RW) {
         const int sh = (int)((o_mu + q * d - avail) & 3);
         double *bq = beta + q * d;
         for (int64_t base = -sh, j0 = 0; base < d; base += 128, j0 += 32) {
@@ -1059,6 +1060,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
                                                                 const double *__restrict__ X,
                                                                 const int64_t *__restrict__ i1,
                                                                 const int64_t *__restrict__ i2, int64_t h,
+                                                                int64_t q0, int64_t q1,
                                                                 Philox ph, uint64_t off, int swap,
                                                                 const double *__restrict__ beta,
                                                                 const uint16_t *__restrict__ flags,
@@ -1093,7 +1095,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
     const int64_t avail = 4 - ph.pos;
     const double eta = V.eta_m + 1.0;
     const int64_t QP = quads_per_pair(d);
-    for (int64_t q = (int64_t)blockIdx.x * RW + (threadIdx.x >> 5); q < h; q += (int64_t)gridDim.x * RW) {
+    for (int64_t q = q0 + (int64_t)blockIdx.x * RW + (threadIdx.x >> 5); q < q1; q += (int64_t)gridDim.x * RW) {
         // row pool (harness): parents at physical rows src_map[i], children into rows dst_rows[r]
         const int64_t p1 = src_map ? src_map[i1[q]] : i1[q];
         const int64_t p2 = src_map ? src_map[i2[q]] : i2[q];
@@ -1371,7 +1373,7 @@ int offspring_m(const temo_problem *prob, const temo_variation *var, const doubl
 
 template <int M>
 int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const int64_t *i1,
-            const int64_t *i2, int64_t h, const Philox &ph, uint64_t off, int gene_swap,
+            const int64_t *i2, int64_t h, int64_t q0, int64_t q1, const Philox &ph, uint64_t off, int gene_swap,
             const double *beta, const uint16_t *flags, double *O, double *FO,
             const int64_t *src_map, const int64_t *dst_rows, size_t sm_a, unsigned grid,
             cudaStream_t s) {
@@ -1380,10 +1382,10 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
         TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a));
     }
     if (prob->id == TEMO_PROB_LSMOP1)
-        k_offspring_apply<M, true><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off, gene_swap,
+        k_offspring_apply<M, true><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off, gene_swap,
                                                               beta, flags, O, FO, 0, src_map, dst_rows);
     else
-        k_offspring_apply<M, false><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, ph, off, gene_swap,
+        k_offspring_apply<M, false><<<grid, RW * 32, sm_a, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off, gene_swap,
                                                                beta, flags, O, FO, 0, src_map, dst_rows);
     return TEMO_OK;
 }
@@ -1396,7 +1398,8 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
                                      const temo_philox_state *, uint64_t, double *, double *, int,    \
                                      bool, size_t, int, cudaStream_t);                                \
     EXT template int apply_m<MM>(const temo_problem *, const VarArgs &, const double *,              \
-                                 const int64_t *, const int64_t *, int64_t, const Philox &, uint64_t, \
+                                 const int64_t *, const int64_t *, int64_t, int64_t, int64_t,         \
+                                 const Philox &, uint64_t,                                             \
                                  int, const double *, const uint16_t *, double *, double *,           \
                                  const int64_t *, const int64_t *, size_t, unsigned, cudaStream_t);
 #ifdef TEMO_M_ONLY
@@ -1515,18 +1518,19 @@ extern "C" size_t temo_offspring_ws_bytes(int64_t h, int64_t d) {
            (size_t)(h * quads_per_pair(d) * sizeof(uint16_t)) + 256;
 }
 
-extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const double *X,
-                                 const int64_t *i1, const int64_t *i2, int64_t h,
-                                 const temo_philox_state *st, uint64_t off, double *O, double *FO,
-                                 const int64_t *src_map, const int64_t *dst_rows,
-                                 void *ws, size_t ws_bytes, temo_stream_t stream) {
+extern "C" int temo_offspring_ws_range(const temo_problem *prob, const temo_variation *var, const double *X,
+                                       const int64_t *i1, const int64_t *i2, int64_t h, int64_t q0, int64_t q1,
+                                       const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                                       const int64_t *src_map, const int64_t *dst_rows,
+                                       void *ws, size_t ws_bytes, temo_stream_t stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !st || !O) return TEMO_EINVAL;
-    if (h == 0) return TEMO_OK;
+    if (q0 < 0 || q1 > h || q0 > q1) return TEMO_EINVAL;
+    if (q1 == q0) return TEMO_OK;
     const int64_t d = prob->d;
     // two-phase path needs congruent streams (one Philox block per quad) and staged constants
     if ((h * d) % 4 != 0 || d > SMAX_D) {
-        if (src_map || dst_rows) return TEMO_EINVAL;  // row maps only on the two-phase path
+        if (src_map || dst_rows || q0 != 0 || q1 != h) return TEMO_EINVAL;  // row maps / ranges: two-phase only
         return launch_offspring(prob, var, X, i1, i2, h, st, off, O, FO, 0, s);
     }
     if (!ws || ws_bytes < temo_offspring_ws_bytes(h, d)) return TEMO_EWORKSPACE;
@@ -1534,14 +1538,14 @@ extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation 
     uint16_t *flags = reinterpret_cast<uint16_t *>(static_cast<char *>(ws) + round_up((int64_t)(h * d * sizeof(double)), 256));
     const Philox ph = philox_from(*st);
     const VarArgs V = var_args(var);
-    const int64_t want = (h + RW - 1) / RW;
+    const int64_t want = (q1 - q0 + RW - 1) / RW;
     stage_begin(S_OFFSPRING, s);
     {
         const unsigned grid = (unsigned)(want < num_sms() * 4 * 8 ? want : num_sms() * 4 * 8);
         if (var->gene_swap)
-            k_offspring_rand<true><<<grid, RW * 32, 0, s>>>(d, V, h, ph, off, 0, beta, flags);
+            k_offspring_rand<true><<<grid, RW * 32, 0, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
         else
-            k_offspring_rand<false><<<grid, RW * 32, 0, s>>>(d, V, h, ph, off, 0, beta, flags);
+            k_offspring_rand<false><<<grid, RW * 32, 0, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
     }
     TEMO_LAUNCH_CHECK();
     stage_end(S_OFFSPRING, s);
@@ -1550,7 +1554,7 @@ extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation 
     const unsigned grid = (unsigned)(want < num_sms() * 3 * 8 ? want : num_sms() * 3 * 8);
 #define APPLY_CASE(MM)                                                                              \
     case MM: {                                                                                      \
-        int rc = apply_m<MM>(prob, V, X, i1, i2, h, ph, off, var->gene_swap, beta, flags, O, FO,   \
+        int rc = apply_m<MM>(prob, V, X, i1, i2, h, q0, q1, ph, off, var->gene_swap, beta, flags, O, FO, \
                              src_map, dst_rows, sm_a, grid, s);                                     \
         if (rc) return rc;                                                                          \
     } break;
@@ -1559,6 +1563,15 @@ extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation 
     TEMO_LAUNCH_CHECK();
     stage_end(S_OFFSPRING_APPLY, s);
     return TEMO_OK;
+}
+
+extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const double *X,
+                                 const int64_t *i1, const int64_t *i2, int64_t h,
+                                 const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                                 const int64_t *src_map, const int64_t *dst_rows,
+                                 void *ws, size_t ws_bytes, temo_stream_t stream) {
+    return temo_offspring_ws_range(prob, var, X, i1, i2, h, 0, h, st, off, O, FO, src_map, dst_rows, ws, ws_bytes,
+                                   stream);
 }
 
 extern "C" int temo_offspring(const temo_problem *prob, const temo_variation *var, const double *X,

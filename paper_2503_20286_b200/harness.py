@@ -186,22 +186,32 @@ class _Stepper:
                               dtype=t.uint8, device=self.dev)
         self.perm = t.empty(self.N, dtype=t.int64, device=self.dev)
         alg = config.algorithm
+        # multi-GPU: one process per GPU, every rank runs the same host RNG stream;
+        # offspring rows and HypE sample columns are sharded, the bitmap ND sort (m >= 4) too
+        import torch.distributed as dist
+
+        self.shard = None
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1 and alg in ("nsga3", "hype"):
+            from .parallel import RowExchange
+
+            self.shard = (dist.get_rank(), dist.get_world_size())
+            self.xchg = RowExchange()
         if alg == "nsga3":
             dist_rank = None
-            import torch.distributed as dist
-
-            if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            if self.shard is not None and m >= 4:  # m <= 3: the staircase sort runs on every rank
                 from .parallel import DistRank
 
-                dist_rank = DistRank(self.N, m, dist.get_rank(), dist.get_world_size(), self.dev)
+                dist_rank = DistRank(self.N, m, self.shard[0], self.shard[1], self.dev)
             self.selector = Nsga3Selector(self.N, m, R, n, self.dev, dist_rank=dist_rank)
         elif alg == "hype":
             from .hype import HypeSelector
+            from .parallel import ColumnExchange
 
             ref = None if config.hv_ref == "auto" else np.asarray(
                 [float(v) for v in str(config.hv_ref).split(",")])
             s = config.hv_samples or 10 * n
-            self.selector = HypeSelector(self.N, m, n, s, ref, self.dev)
+            shard = None if self.shard is None else (self.shard[0], self.shard[1], ColumnExchange())
+            self.selector = HypeSelector(self.N, m, n, s, ref, self.dev, shard=shard)
         elif alg == "rvea":
             from .rvea import RveaSelector
 
@@ -257,15 +267,43 @@ class _Stepper:
         else:  # fused fallback: children into logical rows; make the pool the identity first
             self._pool_identity(st)
             src, dst, obase = None, None, _lib.ptr(cur.X[n:])
-        rc = _lib.lib().temo_offspring_ws(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
-                                          _lib.ptr(self.i12), _lib.ptr(self.i12[h:]), h,
-                                          _lib.sptr(draws.state), off, obase,
-                                          _lib.ptr(cur.F[n:]), src, dst,
-                                          _lib.ptr(self.off_ws), self.off_ws.numel(),
-                                          _lib.stream_handle(self.dev))
+        q0, q1 = 0, h
+        if self.shard is not None and pooled:
+            from .parallel import shard_range
+
+            q0, q1 = shard_range(h, *self.shard)
+        rc = _lib.lib().temo_offspring_ws_range(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
+                                                _lib.ptr(self.i12), _lib.ptr(self.i12[h:]), h, q0, q1,
+                                                _lib.sptr(draws.state), off, obase,
+                                                _lib.ptr(cur.F[n:]), src, dst,
+                                                _lib.ptr(self.off_ws), self.off_ws.numel(),
+                                                _lib.stream_handle(self.dev))
         _lib.check(rc, "offspring")
         draws.commit()
         st.extra["N_cur"] = n + 2 * h
+        if (q0, q1) != (0, h):
+            self._exchange_children(st, n, h)
+
+    def _exchange_children(self, st: DeviceState, n: int, h: int):
+        """Every rank's children (X rows and objectives of its pair range) to every rank: one
+        all-gather of [X | F] rows (NCCL over NVLink), scattered into the replicated pool."""
+        from .parallel import shard_range
+
+        t = _lib.torch()
+        G = self.shard[1]
+        cur = st.cur
+        ranges = [shard_range(h, g, G) for g in range(G)]
+        lo, hi = ranges[self.shard[0]]
+        rows = t.cat([st.phys[n + lo: n + hi], st.phys[n + h + lo: n + h + hi]])
+        logical = t.cat([t.arange(n + lo, n + hi, device=self.dev), t.arange(n + h + lo, n + h + hi, device=self.dev)])
+        local = t.cat([cur.X.index_select(0, rows), cur.F.index_select(0, logical)], dim=1)
+        full = self.xchg(local, [2 * (b - a) for a, b in ranges])
+        all_rows = t.cat([t.cat([st.phys[n + a: n + b], st.phys[n + h + a: n + h + b]]) for a, b in ranges])
+        all_logical = t.cat([t.cat([t.arange(n + a, n + b, device=self.dev), t.arange(n + h + a, n + h + b, device=self.dev)])
+                             for a, b in ranges])
+        d = self.spec.d
+        cur.X.index_copy_(0, all_rows, full[:, :d].contiguous())
+        cur.F.index_copy_(0, all_logical, full[:, d:].contiguous())
 
     def _mutate_in_place(self, st: DeviceState, gen):
         """A shrunken population of one row: O = polynomial_mutation(X) (harness.py:223-226)."""

@@ -120,7 +120,11 @@ class HypeSelector:
     read per call decides whether the Generator advances (the reference draws
     samples only when k >= 1 and the box is non-degenerate)."""
 
-    def __init__(self, N: int, m: int, n: int, s: int, v_ref=None, dev=None):
+    def __init__(self, N: int, m: int, n: int, s: int, v_ref=None, dev=None, shard=None):
+        """``shard = (rank, world, exchange)`` splits the Monte-Carlo work by exchange column
+        (SURVEY 8e): this rank computes columns [C rank / world, C (rank + 1) / world) of the
+        contribution partials and ``exchange(segment, counts)`` all-gathers them (NCCL); the
+        combine then runs the reference's summation order on every rank (bit-identical)."""
         t = _t()
         self.dev = _lib.device(dev)
         self.N, self.m, self.n, self.s = N, m, n, s
@@ -133,6 +137,13 @@ class HypeSelector:
         self.status = t.zeros(1, dtype=t.int32, device=self.dev)
         self.v_ref = None if v_ref is None else t.from_numpy(np.asarray(v_ref, dtype=np.float64)).to(self.dev)
         self.ws_bytes = _lib.lib().temo_hype_select_ws_bytes(N, m, s)
+        self.shard = shard
+        if shard is not None:
+            r, G, _ = shard
+            C = int(_lib.lib().temo_hype_columns(s))
+            self.col_bounds = [(C * g // G, C * (g + 1) // G) for g in range(G)]
+            lo, hi = self.col_bounds[r]
+            self.Tseg = z((max(hi - lo, 1), N), dt=t.float64)
 
     def select(self, F, rng, U=None):
         rank_device(F, self.n, SELECT, self.status, out=(self.rank, self.l, self.nf))
@@ -144,10 +155,24 @@ class HypeSelector:
             st = _lib.sptr(draws.state)
         else:
             st = None
-        rc = L.temo_hype_select(p(F), self.N, self.m, self.n, self.s, p(self.v_ref), p(self.rank), p(self.l),
-                                st, 0, p(U), p(self.keep), p(self.v_hv), p(self.info), p(ws), ws.numel(),
-                                _lib.stream_handle(self.dev))
-        _lib.check(rc, "hype.environmental_selection")
+        sh = _lib.stream_handle(self.dev)
+        if self.shard is None:
+            rc = L.temo_hype_select(p(F), self.N, self.m, self.n, self.s, p(self.v_ref), p(self.rank), p(self.l),
+                                    st, 0, p(U), p(self.keep), p(self.v_hv), p(self.info), p(ws), ws.numel(), sh)
+            _lib.check(rc, "hype.environmental_selection")
+        else:
+            r, G, exchange = self.shard
+            lo, hi = self.col_bounds[r]
+            rc = L.temo_hype_select_begin(p(F), self.N, self.m, self.n, self.s, p(self.v_ref), p(self.rank),
+                                          p(self.l), p(ws), ws.numel(), sh)
+            _lib.check(rc, "hype.environmental_selection")
+            rc = L.temo_hype_select_columns(p(F), self.N, self.m, self.s, lo, hi, st, 0, p(U), p(self.Tseg),
+                                            p(ws), ws.numel(), sh)
+            _lib.check(rc, "hype.environmental_selection")
+            Tg = exchange(self.Tseg[: hi - lo], [b - a for a, b in self.col_bounds])
+            rc = L.temo_hype_select_end(p(F), self.N, self.m, self.n, self.s, p(self.rank), p(self.l), p(Tg),
+                                        p(self.keep), p(self.v_hv), p(self.info), p(ws), ws.numel(), sh)
+            _lib.check(rc, "hype.environmental_selection")
         self.info_host.copy_(self.info, non_blocking=True)
         _lib.torch().cuda.current_stream(self.dev).synchronize()
         if U is None and int(self.info_host[3]):

@@ -1,4 +1,15 @@
-"""Multi-GPU ND sort: column-sharded dominance with a per-front mask all-gather.
+"""Multi-GPU plumbing: row-sharded offspring, column-sharded HypE sampling, and the
+column-sharded bitmap ND sort (m >= 4) with a per-front mask all-gather.
+
+Sharding used by the generation loop (harness._Stepper under torch.distributed):
+  * offspring + evaluation: rank g computes the pairs ``shard_range(h, g, G)`` with exactly the
+    draws the full call gives them (temo_offspring_ws_range), then ``RowExchange`` all-gathers
+    the children's X rows and objective rows so every rank holds the merged population;
+  * HypE: rank g computes its range of Monte-Carlo exchange columns; ``ColumnExchange``
+    all-gathers them and every rank combines in the reference's order (bit-identical);
+  * ND sort: m <= 3 runs the staircase sort on every rank (latency-bound, ~1 ms); m >= 4 shards
+    the O(N^2) bitmap by column tiles (DistRank below).
+
 
 One process per GPU (``torch.distributed``, NCCL over NVLink).  Every rank
 holds the same objectives F, runs K0 identically and owns a contiguous range
@@ -23,6 +34,52 @@ import numpy as np
 from . import _lib
 
 SORT, SELECT = 0, 1
+
+
+def all_gather_into(recv, send, group=None):
+    """``dist.all_gather_into_tensor`` (NCCL over NVLink on GPUs).  Under gloo (CPU tests, or
+    several ranks sharing one GPU in the sharding parity test) CUDA buffers are staged through
+    host memory, since gloo's all-gather runs on host tensors."""
+    import torch.distributed as dist
+
+    if recv.is_cuda and dist.get_backend(group) == "gloo":
+        r = recv.cpu()
+        dist.all_gather_into_tensor(r, send.cpu(), group=group)
+        recv.copy_(r)
+    else:
+        dist.all_gather_into_tensor(recv, send, group=group)
+
+
+def shard_range(total: int, rank: int, world: int):
+    """[lo, hi) of an even split of range(total) (rank g of world G)."""
+    return total * rank // world, total * (rank + 1) // world
+
+
+class RowExchange:
+    """All-gather of per-rank row blocks of unequal length (padded to the longest for NCCL's
+    all_gather_into_tensor); returns the concatenation in rank order."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.buf = {}
+
+    def __call__(self, local, counts):
+        t = _lib.torch()
+        G = len(counts)
+        mx = max(max(counts), 1)
+        tail = tuple(local.shape[1:])
+        key = (mx, tail, local.dtype, str(local.device))
+        if key not in self.buf:
+            self.buf[key] = (t.zeros((mx,) + tail, dtype=local.dtype, device=local.device),
+                             t.zeros((G * mx,) + tail, dtype=local.dtype, device=local.device))
+        send, recv = self.buf[key]
+        send[: local.shape[0]].copy_(local)
+        all_gather_into(recv, send, self.group)
+        return t.cat([recv[g * mx: g * mx + c] for g, c in enumerate(counts)])
+
+
+class ColumnExchange(RowExchange):
+    """HypE exchange columns: per-rank (columns x N) blocks -> the full column-major (C x N) buffer."""
 
 
 def shard_bounds(N: int, G: int):
@@ -106,11 +163,9 @@ class TorchDistExchange:
         self.full = t.zeros(W, dtype=t.int32, device=device)
 
     def __call__(self, seg):
-        import torch.distributed as dist
-
         self.send.zero_()
         self.send[: seg.numel()].copy_(seg)
-        dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+        all_gather_into(self.recv, self.send, self.group)
         for g, (lo, hi) in enumerate(self.bounds):
             n = 8 * (hi - lo)
             if n:

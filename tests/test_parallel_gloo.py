@@ -129,3 +129,51 @@ def test_shard_bounds_cover_and_balance():
             if nT // 4 >= 8 * G:
                 area = [sum(t + 1 for t in range(lo, hi)) for lo, hi in b]
                 assert max(area) / (sum(area) / G) < 1.15
+
+
+def _row_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_20286_b200.parallel import ColumnExchange, RowExchange, shard_range
+
+    out = []
+    for total, width in ((11, 5), (2, 3), (1000, 13)):
+        ranges = [shard_range(total, g, world) for g in range(world)]
+        lo, hi = ranges[rank]
+        local = torch.arange(lo * width, hi * width, dtype=torch.float64).reshape(hi - lo, width)
+        ex = RowExchange() if total % 2 else ColumnExchange()
+        full = ex(local, [b - a for a, b in ranges])
+        full2 = ex(local, [b - a for a, b in ranges])  # buffers reused
+        out.append((full.numpy().copy(), full2.numpy().copy()))
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_exchange_uneven(world):
+    """RowExchange / ColumnExchange: padded all-gather of unequal per-rank blocks, rank order."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_row_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for ci, (total, width) in enumerate(((11, 5), (2, 3), (1000, 13))):
+        want = np.arange(total * width, dtype=np.float64).reshape(total, width)
+        for r in range(world):
+            assert np.array_equal(res[r][ci][0], want) and np.array_equal(res[r][ci][1], want)
+
+
+def test_shard_range_partition():
+    from paper_2503_20286_b200.parallel import shard_range
+
+    for total in (0, 1, 7, 100_000, 100_001):
+        for G in (1, 2, 3, 8):
+            rs = [shard_range(total, g, G) for g in range(G)]
+            assert rs[0][0] == 0 and rs[-1][1] == total
+            assert all(rs[g][1] == rs[g + 1][0] for g in range(G - 1))
+            assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
