@@ -192,7 +192,8 @@ typedef struct temo_philox_host {
 int temo_host_permutation(temo_philox_host *st, int64_t n, int64_t *out);
 
 #define TEMO_PROB_DTLZ1 1 /* ... TEMO_PROB_DTLZ1 + 6 = DTLZ7 (problems.py:105-136) */
-#define TEMO_PROB_LSMOP1 101 /* LSMOP1, Cheng et al. 2017 (no reference; self-oracle) */
+#define TEMO_PROB_LSMOP1 101 /* LSMOP1 ... TEMO_PROB_LSMOP1 + 8 = LSMOP9: Cheng et al. 2017 in the */
+#define TEMO_PROB_LSMOP9 109 /* PlatEMO form (no reference; self-oracle oracle/problems.py) */
 
 typedef struct temo_problem {
     int32_t id;          /* TEMO_PROB_* */
@@ -210,9 +211,13 @@ typedef struct temo_variation {
     const double *lower, *upper; /* device, length d */
 } temo_variation;
 
-/* problems.evaluate (problems.py:105-136; LSMOP1 new): F (n x m) = f(X (n x d)) */
+/* problems.evaluate (problems.py:105-136; LSMOP1-9 new): F (n x m) = f(X (n x d)) */
 int temo_evaluate(const temo_problem *prob, const double *X, int64_t n, double *F,
                   temo_stream_t stream);
+/* Same, for rows gathered through a map: F[r] = f(X[rows[r]]) (rows NULL = identity); the
+ * row-pool layout of the generation loop (children at physical pool rows). */
+int temo_evaluate_rows(const temo_problem *prob, const double *X, const int64_t *rows, int64_t n,
+                       double *F, temo_stream_t stream);
 
 /* SBX spread factor (variation.py:77-78) for U = mu[t]: beta[t] = pow(2 mu, e) or
  * pow(1 / (2 - 2 mu), e), e = 1 / (eta_c + 1); fast = 1 uses the exp/log form the fused

@@ -1,10 +1,10 @@
-"""Oracle: DTLZ1-7 (restates ``temo/problems.py``) and LSMOP1 (self-oracle). Test infrastructure only.
+"""Oracle: DTLZ1-7 (restates ``temo/problems.py``) and LSMOP1-9 (self-oracle). Test infrastructure only.
 
 DTLZ parity vs the reference is by tolerance (1e-5 rel, BASELINE north star):
 NumPy's vectorised cos/sin/pow and CUDA's differ in the last ulp.
 
-LSMOP1 has no reference implementation (problems.py:18): this is a
-NumPy restatement of the standard definition (Cheng et al. 2017, cited at
+LSMOP1-9 have no reference implementation (problems.py:18): this is a
+NumPy restatement of the standard definitions (Cheng et al. 2017, cited at
 PAPER.md:518) in the PlatEMO formulation -- *parity unpinned*.
 """
 
@@ -139,7 +139,69 @@ def evaluate_lsmop1(X, m, nk=5):
     return (1.0 + G) * head * tail
 
 
+# LSMOP1-9 (Cheng, Jin, Olhofer, Sendhoff 2017, "Test problems for large-scale multiobjective
+# and many-objective optimization", IEEE T-Cyb 47(12)), restated from the PlatEMO
+# formulation (LSMOP*.m CalObj): eta1 on odd objectives, eta2 on even ones.
+_ETA = {1: ("sphere", "sphere"), 2: ("griewank", "schwefel"), 3: ("rastrigin", "rosenbrock"),
+        4: ("ackley", "griewank"), 5: ("sphere", "sphere"), 6: ("rosenbrock", "schwefel"),
+        7: ("ackley", "rosenbrock"), 8: ("griewank", "sphere"), 9: ("sphere", "ackley")}
+
+
+def _eta(fn, z):
+    L = z.shape[1]
+    if fn == "sphere":
+        return np.sum(z ** 2, axis=1)
+    if fn == "griewank":
+        return np.sum(z ** 2, axis=1) / 4000.0 - np.prod(np.cos(z / np.sqrt(np.arange(1, L + 1))), axis=1) + 1.0
+    if fn == "schwefel":
+        return np.max(np.abs(z), axis=1)
+    if fn == "rastrigin":
+        return np.sum(z ** 2 - 10.0 * np.cos(2.0 * np.pi * z) + 10.0, axis=1)
+    if fn == "rosenbrock":
+        return np.sum(100.0 * (z[:, :-1] ** 2 - z[:, 1:]) ** 2 + (z[:, :-1] - 1.0) ** 2, axis=1)
+    if fn == "ackley":
+        return (20.0 - 20.0 * np.exp(-0.2 * np.sqrt(np.sum(z ** 2, axis=1) / L))
+                - np.exp(np.sum(np.cos(2.0 * np.pi * z), axis=1) / L) + np.exp(1.0))
+    raise ValueError(fn)
+
+
+def evaluate_lsmop(k, X, m, nk=5):
+    """LSMOP k: linkage (linear k <= 4, cos k >= 5), per-subcomponent eta, front linear (1-4),
+    concave (5-8: (1 + G_i + G_{i+1}) cos/sin) or disconnected (9)."""
+    if k == 1:
+        return evaluate_lsmop1(X, m, nk)
+    X = np.asarray(X, dtype=np.float64)
+    n, d = X.shape
+    sublen, offset = lsmop_groups_for(m, d, nk)
+    idx = np.arange(m, d + 1, dtype=np.float64) / d
+    c = np.cos(idx * np.pi / 2.0) if k >= 5 else idx
+    xs = (1.0 + c) * X[:, m - 1:] - 10.0 * X[:, :1]
+    G = np.zeros((n, m))
+    for i in range(m):
+        fn = _ETA[k][i % 2]
+        for j in range(nk):
+            a = offset[i] + j * sublen[i]
+            G[:, i] = G[:, i] + _eta(fn, xs[:, a:a + sublen[i]])
+    G = G / sublen / nk
+    ones = np.ones((n, 1))
+    if k <= 4:
+        head = np.cumprod(np.concatenate([ones, X[:, : m - 1]], axis=1), axis=1)[:, ::-1]
+        tail = np.concatenate([ones, 1.0 - X[:, m - 2::-1]], axis=1)
+        return (1.0 + G) * head * tail
+    if k <= 8:
+        head = np.cumprod(np.concatenate([ones, np.cos(X[:, : m - 1] * np.pi / 2.0)], axis=1), axis=1)[:, ::-1]
+        tail = np.concatenate([ones, np.sin(X[:, m - 2::-1] * np.pi / 2.0)], axis=1)
+        Gn = np.concatenate([G[:, 1:], np.zeros((n, 1))], axis=1)
+        return (1.0 + G + Gn) * head * tail
+    Gs = 1.0 + np.sum(G, axis=1)
+    F = np.empty((n, m))
+    F[:, : m - 1] = X[:, : m - 1]
+    F[:, m - 1] = (1.0 + Gs) * (m - np.sum(F[:, : m - 1] / (1.0 + Gs)[:, None]
+                                         * (1.0 + np.sin(3.0 * np.pi * F[:, : m - 1])), axis=1))
+    return F
+
+
 def evaluate(name, X, m):
-    if name == "lsmop1":
-        return evaluate_lsmop1(X, m)
+    if name.startswith("lsmop"):
+        return evaluate_lsmop(int(name[5:]), X, m)
     return evaluate_dtlz(name, X, m)

@@ -69,6 +69,7 @@ SIGNATURES = {
     "temo_gather_rows2": (_I32, [_P, _P, _P, _I64, _I64, _P, _P]),
     "temo_neighbors": (_I32, [_P, _I64, _I32, _I32, _P, _P]),
     "temo_evaluate": (_I32, [_P, _P, _I64, _P, _P]),
+    "temo_evaluate_rows": (_I32, [_P, _P, _P, _I64, _P, _P]),
     "temo_uniform": (_I32, [_P, _U64, _I64, _P, _P]),
     "temo_sbx_beta": (_I32, [_P, _I64, _D, _I32, _P, _P]),
     "temo_sbx": (_I32, [_P, _P, _P, _I64, _I64, _P, _U64, _P, _P, _P, _P, _P]),

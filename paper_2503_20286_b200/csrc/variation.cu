@@ -194,14 +194,141 @@ __device__ void eval_row(const temo_problem &P, const double *x, double *f, doub
 
 template <int M>
 __global__ void __launch_bounds__(VT) k_evaluate(temo_problem P, const double *__restrict__ X,
-                                                 int64_t n, double *__restrict__ F) {
+                                                 const int64_t *__restrict__ map, int64_t lo1, int64_t c1,
+                                                 int64_t lo2, int64_t c2, double *__restrict__ F) {
     __shared__ double red[VT / 32];
     __shared__ double f[16];
-    const int64_t r = blockIdx.x;
-    if (r >= n) return;
-    eval_row<M>(P, X + r * P.d, f, red);
+    const int64_t w = blockIdx.x;
+    if (w >= c1 + c2) return;
+    const int64_t r = w < c1 ? lo1 + w : lo2 + (w - c1);
+    eval_row<M>(P, X + (map ? map[r] : r) * P.d, f, red);
     __syncthreads();
     if (threadIdx.x < M) F[r * M + threadIdx.x] = f[threadIdx.x];
+}
+
+// ------------------------------------------------------------------ LSMOP2..9
+// Cheng et al. 2017 in the PlatEMO formulation (no reference implementation; self-oracle
+// oracle/problems.py evaluate_lsmop).  Objective i (0-based) sums its nk subcomponents of
+// x^s through eta1 (even i, PlatEMO's odd objectives) or eta2 (odd i); linkage
+// z = (1 + c(j)) x_j - 10 x_1 with c = j/D (LSMOP1-4) or cos(j/D pi/2) (LSMOP5-9).
+enum LsFn { LS_SPHERE, LS_GRIEWANK, LS_SCHWEFEL, LS_RASTRIGIN, LS_ROSENBROCK, LS_ACKLEY };
+
+__device__ __forceinline__ int lsmop_fn(int k, int i) {
+    const bool odd = i & 1;  // PlatEMO's even-numbered objective: eta2
+    switch (k) {
+        case 2: return odd ? LS_SCHWEFEL : LS_GRIEWANK;
+        case 3: return odd ? LS_ROSENBROCK : LS_RASTRIGIN;
+        case 4: return odd ? LS_GRIEWANK : LS_ACKLEY;
+        case 6: return odd ? LS_SCHWEFEL : LS_ROSENBROCK;
+        case 7: return odd ? LS_ROSENBROCK : LS_ACKLEY;
+        case 8: return odd ? LS_SPHERE : LS_GRIEWANK;
+        case 9: return odd ? LS_ACKLEY : LS_SPHERE;
+        default: return LS_SPHERE;  // LSMOP1, LSMOP5
+    }
+}
+
+__device__ __forceinline__ double lsmop_link(int k, int64_t g, int64_t d, double x, double x0) {
+    const double j = (double)(g + 1) / (double)d;  // PlatEMO's (M:D)./D
+    const double c = k >= 5 ? cos(j * PI / 2.0) : j;
+    return (1.0 + c) * x - 10.0 * x0;
+}
+
+// One warp per row; logical rows [lo1, lo1 + c1) then [lo2, lo2 + c2); row l is read from
+// X + (map ? map[l] : l) * d and written to F + l * M.
+template <int M>
+__global__ void __launch_bounds__(256) k_eval_lsmop(temo_problem P, const double *__restrict__ X,
+                                                    const int64_t *__restrict__ map, int64_t lo1, int64_t c1,
+                                                    int64_t lo2, int64_t c2, double *__restrict__ F) {
+    const int lane = threadIdx.x & 31;
+    const int64_t d = P.d, nrow = c1 + c2;
+    const int k = P.id - TEMO_PROB_LSMOP1 + 1;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nrow;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t l = w < c1 ? lo1 + w : lo2 + (w - c1);
+        const double *x = X + (map ? map[l] : l) * d;
+        const double x0 = x[0];
+        double G[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const int fn = lsmop_fn(k, i);
+            const int64_t L = P.sublen[i];
+            double gi = 0.0;
+            for (int j = 0; j < P.nk; ++j) {
+                const int64_t start = (M - 1) + P.offset[i] + j * L;
+                double s2 = 0.0, sc = 0.0, pr = 1.0, mx = 0.0;
+                for (int64_t t = lane; t < L; t += 32) {
+                    const int64_t g = start + t;
+                    const double z = lsmop_link(k, g, d, x[g], x0);
+                    switch (fn) {
+                        case LS_SPHERE: s2 += z * z; break;
+                        case LS_GRIEWANK:
+                            s2 += z * z;
+                            pr *= cos(z / sqrt((double)(t + 1)));
+                            break;
+                        case LS_SCHWEFEL: mx = fmax(mx, fabs(z)); break;
+                        case LS_RASTRIGIN: s2 += z * z - 10.0 * cos(2.0 * PI * z) + 10.0; break;
+                        case LS_ROSENBROCK:
+                            if (t + 1 < L) {
+                                const double z2 = lsmop_link(k, g + 1, d, x[g + 1], x0);
+                                const double a = z * z - z2, b = z - 1.0;
+                                s2 += 100.0 * (a * a) + b * b;
+                            }
+                            break;
+                        default:  // LS_ACKLEY
+                            s2 += z * z;
+                            sc += cos(2.0 * PI * z);
+                            break;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    s2 += __shfl_xor_sync(~0u, s2, o);
+                    sc += __shfl_xor_sync(~0u, sc, o);
+                    pr *= __shfl_xor_sync(~0u, pr, o);
+                    mx = fmax(mx, __shfl_xor_sync(~0u, mx, o));
+                }
+                double v;
+                if (fn == LS_GRIEWANK) v = s2 / 4000.0 - pr + 1.0;
+                else if (fn == LS_SCHWEFEL) v = mx;
+                else if (fn == LS_ACKLEY)
+                    v = 20.0 - 20.0 * exp(-0.2 * sqrt(s2 / (double)L)) - exp(sc / (double)L) + exp(1.0);
+                else v = s2;
+                gi += v;
+            }
+            G[i] = gi / (double)L / (double)P.nk;
+        }
+        if (lane != 0) continue;
+        double *f = F + l * M;
+        if (k <= 4) {  // linear front (LSMOP1-4)
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                double head = 1.0;
+                for (int q = 0; q < M - 1 - i; ++q) head = head * x[q];
+                const double tail = i == 0 ? 1.0 : 1.0 - x[M - 1 - i];
+                f[i] = (1.0 + G[i]) * head * tail;
+            }
+        } else if (k <= 8) {  // concave front (LSMOP5-8): (1 + G_i + G_{i+1})
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                double head = 1.0;
+                for (int q = 0; q < M - 1 - i; ++q) head = head * cos(x[q] * PI / 2.0);
+                const double tail = i == 0 ? 1.0 : sin(x[M - 1 - i] * PI / 2.0);
+                const double gn = i + 1 < M ? G[i + 1] : 0.0;
+                f[i] = (1.0 + G[i] + gn) * head * tail;
+            }
+        } else {  // LSMOP9: disconnected front
+            double gs = 0.0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) gs += G[i];
+            gs = 1.0 + gs;
+            double hsum = 0.0;
+            for (int q = 0; q < M - 1; ++q) {
+                f[q] = x[q];
+                hsum += x[q] / (1.0 + gs) * (1.0 + sin(3.0 * PI * x[q]));
+            }
+            f[M - 1] = (1.0 + gs) * ((double)M - hsum);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ fused offspring
@@ -1307,7 +1434,7 @@ static VarArgs var_args(const temo_variation *v) {
 
 static bool prob_ok(const temo_problem *p) {
     if (!p || p->m < 2 || p->m > 16 || p->d < p->m) return false;
-    if (p->id == TEMO_PROB_LSMOP1) return p->nk >= 1;
+    if (p->id >= TEMO_PROB_LSMOP1 && p->id <= TEMO_PROB_LSMOP9) return p->nk >= 1;
     return p->id >= 1 && p->id <= 7;
 }
 
@@ -1331,8 +1458,17 @@ static Philox philox_or_zero(const temo_philox_state *st) {
 // count with -DTEMO_M_ONLY=M; each per-M unit instantiates only its M (the
 // base unit declares them extern), so the M-templated kernels build in parallel.
 template <int M>
-int eval_m(const temo_problem *prob, const double *X, int64_t n, double *F, cudaStream_t s) {
-    k_evaluate<M><<<(unsigned)n, VT, 0, s>>>(*prob, X, n, F);
+int eval_m(const temo_problem *prob, const double *X, const int64_t *map, int64_t lo1, int64_t c1, int64_t lo2,
+           int64_t c2, double *F, cudaStream_t s) {
+    const int64_t n = c1 + c2;
+    if (n <= 0) return TEMO_OK;
+    if (prob->id > TEMO_PROB_LSMOP1) {  // LSMOP2..9: warp per row
+        const int64_t want = (n + 7) / 8;
+        const unsigned grid = (unsigned)(want < num_sms() * 8 * 4 ? want : num_sms() * 8 * 4);
+        k_eval_lsmop<M><<<grid, 256, 0, s>>>(*prob, X, map, lo1, c1, lo2, c2, F);
+    } else {
+        k_evaluate<M><<<(unsigned)n, VT, 0, s>>>(*prob, X, map, lo1, c1, lo2, c2, F);
+    }
     return TEMO_OK;
 }
 
@@ -1392,7 +1528,8 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
 
 #define TEMO_M_LIST(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 #define TEMO_VAR_DECL(MM, EXT)                                                                      \
-    EXT template int eval_m<MM>(const temo_problem *, const double *, int64_t, double *, cudaStream_t); \
+    EXT template int eval_m<MM>(const temo_problem *, const double *, const int64_t *, int64_t, int64_t,     \
+                                int64_t, int64_t, double *, cudaStream_t);                                  \
     EXT template int offspring_m<MM>(const temo_problem *, const temo_variation *, const double *,   \
                                      const int64_t *, const int64_t *, int64_t,                      \
                                      const temo_philox_state *, uint64_t, double *, double *, int,    \
@@ -1415,16 +1552,36 @@ using namespace temo;
 
 #ifndef TEMO_M_ONLY
 
+// objectives of logical rows [lo1, lo1 + c1) u [lo2, lo2 + c2) (row l read at map[l], written to F + l m)
+static int eval_rows(const temo_problem *prob, const double *X, const int64_t *map, int64_t lo1, int64_t c1,
+                     int64_t lo2, int64_t c2, double *F, cudaStream_t s) {
+#define EVAL_CASE(MM) case MM: { int rc = eval_m<MM>(prob, X, map, lo1, c1, lo2, c2, F, s); if (rc) return rc; } break;
+    TEMO_M_SWITCH(prob->m, EVAL_CASE)
+#undef EVAL_CASE
+    TEMO_LAUNCH_CHECK();
+    return TEMO_OK;
+}
+
 extern "C" int temo_evaluate(const temo_problem *prob, const double *X, int64_t n, double *F,
                              temo_stream_t stream) {
     if (!prob_ok(prob) || n < 0 || !X || !F) return TEMO_EINVAL;
     if (n == 0) return TEMO_OK;
     cudaStream_t s = (cudaStream_t)stream;
     stage_begin(S_EVALUATE, s);
-#define EVAL_CASE(MM) case MM: { int rc = eval_m<MM>(prob, X, n, F, s); if (rc) return rc; } break;
-    TEMO_M_SWITCH(prob->m, EVAL_CASE)
-#undef EVAL_CASE
-    TEMO_LAUNCH_CHECK();
+    const int rc = eval_rows(prob, X, nullptr, 0, n, 0, 0, F, s);
+    if (rc) return rc;
+    stage_end(S_EVALUATE, s);
+    return TEMO_OK;
+}
+
+extern "C" int temo_evaluate_rows(const temo_problem *prob, const double *X, const int64_t *rows, int64_t n,
+                                  double *F, temo_stream_t stream) {
+    if (!prob_ok(prob) || n < 0 || !X || !F) return TEMO_EINVAL;
+    if (n == 0) return TEMO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    stage_begin(S_EVALUATE, s);
+    const int rc = eval_rows(prob, X, rows, 0, n, 0, 0, F, s);
+    if (rc) return rc;
     stage_end(S_EVALUATE, s);
     return TEMO_OK;
 }
@@ -1487,6 +1644,9 @@ extern "C" int temo_pm(const temo_variation *var, const double *X, int64_t rows,
     return TEMO_OK;
 }
 
+// LSMOP2..9 are evaluated by a separate warp-per-row pass over the children (no fused sums)
+static bool fused_eval(const temo_problem *prob) { return prob->id <= TEMO_PROB_LSMOP1; }
+
 static int launch_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
                             const int64_t *i1, const int64_t *i2, int64_t h,
                             const temo_philox_state *st, uint64_t off, double *O, double *FO,
@@ -1498,16 +1658,21 @@ static int launch_offspring(const temo_problem *prob, const temo_variation *var,
     const size_t smem = smem_rows ? 2 * d * sizeof(double) : 0;
     // warp-per-pair kernel whenever every stream is congruent mod 4 (one Philox block per quad)
     const bool warp_path = (h * d) % 4 == 0 && !offspring_cta_forced();
+    double *FOk = fused_eval(prob) ? FO : nullptr;
     stage_begin(S_OFFSPRING, s);
-#define OFF_CASE(MM)                                                                              \
-    case MM: {                                                                                    \
-        int rc = offspring_m<MM>(prob, var, X, i1, i2, h, st, off, O, FO, single, warp_path, smem, \
-                                 smem_rows, s);                                                   \
-        if (rc) return rc;                                                                        \
+#define OFF_CASE(MM)                                                                               \
+    case MM: {                                                                                     \
+        int rc = offspring_m<MM>(prob, var, X, i1, i2, h, st, off, O, FOk, single, warp_path, smem, \
+                                 smem_rows, s);                                                    \
+        if (rc) return rc;                                                                         \
     } break;
     TEMO_M_SWITCH(prob->m, OFF_CASE)
 #undef OFF_CASE
     TEMO_LAUNCH_CHECK();
+    if (FO && !FOk) {
+        const int rc = eval_rows(prob, O, nullptr, 0, single ? h : 2 * h, 0, 0, FO, s);
+        if (rc) return rc;
+    }
     stage_end(S_OFFSPRING, s);
     return TEMO_OK;
 }
@@ -1552,15 +1717,20 @@ extern "C" int temo_offspring_ws_range(const temo_problem *prob, const temo_vari
     stage_begin(S_OFFSPRING_APPLY, s);
     const size_t sm_a = 3 * d * sizeof(double) + d + 16;
     const unsigned grid = (unsigned)(want < num_sms() * 3 * 8 ? want : num_sms() * 3 * 8);
+    double *FOk = fused_eval(prob) ? FO : nullptr;
 #define APPLY_CASE(MM)                                                                              \
     case MM: {                                                                                      \
-        int rc = apply_m<MM>(prob, V, X, i1, i2, h, q0, q1, ph, off, var->gene_swap, beta, flags, O, FO, \
+        int rc = apply_m<MM>(prob, V, X, i1, i2, h, q0, q1, ph, off, var->gene_swap, beta, flags, O, FOk, \
                              src_map, dst_rows, sm_a, grid, s);                                     \
         if (rc) return rc;                                                                          \
     } break;
     TEMO_M_SWITCH(prob->m, APPLY_CASE)
 #undef APPLY_CASE
     TEMO_LAUNCH_CHECK();
+    if (FO && !FOk) {  // children of pairs [q0, q1): logical rows q and h + q
+        const int rc = eval_rows(prob, O, dst_rows, q0, q1 - q0, h + q0, q1 - q0, FO, s);
+        if (rc) return rc;
+    }
     stage_end(S_OFFSPRING_APPLY, s);
     return TEMO_OK;
 }

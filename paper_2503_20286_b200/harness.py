@@ -158,6 +158,17 @@ class DeviceState:
         return self.cur.F[: self.n]
 
 
+@dataclass
+class HostInputs:
+    """One generation's host-drawn inputs: the parent pairing i1 ++ i2 (2h int64), the Philox
+    state + offset of the offspring's device uniforms, and NSGA-III's shuffle permutation."""
+
+    i12: object
+    state: object
+    off: int
+    shuffle: object = None
+
+
 class _Stepper:
     """Per-algorithm generation step on the device (harness.py:164-248)."""
 
@@ -249,16 +260,43 @@ class _Stepper:
         return st
 
     # -- offspring of NSGA-III / HypE / RVEA (harness.py:201-204, 218-222) into rows [n, N)
-    def _offspring(self, st: DeviceState, gen):
+    def draw_host_inputs(self, gen, n: int | None = None, shuffle: bool = True) -> HostInputs:
+        """The host Generator's part of one NSGA-III / HypE / RVEA generation, drawn in the
+        reference's order (harness.py:201-204 pairing permutation, the offspring's uniforms
+        reserved for the device, then the NSGA-III shuffle permutation nsga3.py:190)."""
+        n = self.n if n is None else n
+        h = n // 2
+        p = rng_permutation(gen, n)
+        draws = DeviceDraws(gen)
+        hd = h * self.spec.d
+        off = draws.take((3 if self.params.gene_swap else 1) * hd + 4 * hd)
+        state = draws.state
+        draws.commit()
+        perm = rng_permutation(gen, n + 2 * h) if shuffle and self.config.algorithm == "nsga3" else None
+        return HostInputs(p[: 2 * h].astype(np.int64), state, off, perm)
+
+    def upload_host_inputs(self, inputs: list) -> list:
+        """Device-resident copies of pre-drawn host inputs (bench: inputs in HBM before timing)."""
+        t = _lib.torch()
+        out = []
+        for hi in inputs:
+            i12 = t.from_numpy(hi.i12).to(self.dev)
+            sh = None if hi.shuffle is None else t.from_numpy(hi.shuffle.astype(np.int64)).to(self.dev)
+            out.append(HostInputs(i12, hi.state, hi.off, sh))
+        return out
+
+    def _offspring(self, st: DeviceState, gen, pre: HostInputs | None = None):
         n = st.n  # RVEA's population is the number of non-empty partitions (<= self.n)
         if n < 2:
             return self._mutate_in_place(st, gen)
         h = n // 2
-        i1, i2 = (lambda p, hh: (p[:hh], p[hh: 2 * hh]))(rng_permutation(gen, n), h)
-        self.ring.upload(np.concatenate([i1, i2]).astype(np.int64), self.i12[: 2 * h])
-        draws = DeviceDraws(gen)
-        hd = h * self.spec.d
-        off = draws.take((3 if self.params.gene_swap else 1) * hd + 4 * hd)
+        if pre is None:
+            pre = self.draw_host_inputs(gen, n, shuffle=False)
+            self.ring.upload(pre.i12, self.i12[: 2 * h])
+            i12 = self.i12
+        else:
+            i12 = pre.i12
+        off = pre.off
         cur = st.cur
         pooled = ((h * self.spec.d) % 4 == 0 and self.spec.d <= 3000  # two-phase path (row maps)
                   and not getattr(self, "force_unpooled", False))
@@ -273,13 +311,12 @@ class _Stepper:
 
             q0, q1 = shard_range(h, *self.shard)
         rc = _lib.lib().temo_offspring_ws_range(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
-                                                _lib.ptr(self.i12), _lib.ptr(self.i12[h:]), h, q0, q1,
-                                                _lib.sptr(draws.state), off, obase,
+                                                _lib.ptr(i12), _lib.ptr(i12[h:]), h, q0, q1,
+                                                _lib.sptr(pre.state), off, obase,
                                                 _lib.ptr(cur.F[n:]), src, dst,
                                                 _lib.ptr(self.off_ws), self.off_ws.numel(),
                                                 _lib.stream_handle(self.dev))
         _lib.check(rc, "offspring")
-        draws.commit()
         st.extra["N_cur"] = n + 2 * h
         if (q0, q1) != (0, h):
             self._exchange_children(st, n, h)
@@ -345,12 +382,15 @@ class _Stepper:
         """X of the current offspring (logical rows [n, N))."""
         return st.rows(st.n, st.extra.get("N_cur", self.N))
 
-    def step(self, st: DeviceState, g: int, gen, timed: bool = True):
+    def step(self, st: DeviceState, g: int, gen, timed: bool = True, pre: HostInputs | None = None):
         """One generation (harness.py:206-248); returns (state, seconds).
 
         ``seconds`` is the device time of the whole step -- or of the selection alone with
         ``time_selection_only`` -- from CUDA events on the launching stream (the call waits for
-        the step).  ``timed=False`` returns at once with ``seconds = None`` (launch-ahead loops)."""
+        the step).  ``timed=False`` returns at once with ``seconds = None`` (launch-ahead loops).
+        ``pre``: this generation's host inputs drawn ahead by ``draw_host_inputs`` and made
+        device-resident by ``upload_host_inputs`` (NSGA-III; the Generator must already be past
+        them)."""
         t = _lib.torch()
         alg = self.config.algorithm
         ev = [t.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
@@ -362,15 +402,23 @@ class _Stepper:
                 ev[1].record()
                 ev[2].record()
         else:
-            self._offspring(st, gen)
+            if pre is not None and alg != "nsga3":
+                raise ValueError("pre-drawn host inputs are supported for NSGA-III only")
+            if pre is None:
+                self._offspring(st, gen)
+            else:
+                self._offspring(st, gen, pre)
             if timed:
                 ev[1].record()
             cur, nxt = st.cur, st.nxt
             n = self.n
             if alg == "nsga3":
-                self.ring.upload(rng_permutation(gen, self.N), self.perm)
-                keep = self.selector.select(cur.F, self.perm)
-                self._pool_update(st, self.perm, keep)  # survivors' X rows stay where they are
+                if pre is None:  # nsga3.py:190 shuffle, drawn after the offspring's uniforms
+                    perm = self.ring.upload(rng_permutation(gen, self.N), self.perm)
+                else:
+                    perm = pre.shuffle
+                keep = self.selector.select(cur.F, perm)
+                self._pool_update(st, perm, keep)  # survivors' X rows stay where they are
                 _lib.gather_rows(self.selector.Fs, keep, nxt.F[:n])
             elif alg == "hype":  # no shuffle (hype.py:135-163)
                 keep = self.selector.select(cur.F, gen)

@@ -1,13 +1,16 @@
-"""Benchmark problems -- drop-in for ``temo.problems`` (problems.py:21-184) plus LSMOP1.
+"""Benchmark problems -- drop-in for ``temo.problems`` (problems.py:21-184) plus LSMOP1-9.
 
 Evaluation runs on the GPU (``temo_evaluate``; fused into offspring generation
-by ``temo_offspring``).  DTLZ1-7 follow problems.py:69-136 op for op; results
-agree with NumPy to the last few ulps (transcendentals differ), inside the
-north star's 1e-5 relative tolerance.  LSMOP1 is new (the reference has no
-LSMOP): the standard definition of Cheng et al. 2017 in the PlatEMO
-formulation -- linear linkage x^s_i <- (1 + i/D) x^s_i - 10 x_1, chaotic
-subcomponent sizes (c <- 3.8 c (1 - c), nk = 5), Sphere g on every group and
-the linear front.  As in PlatEMO, the requested dimension only sizes the
+by ``temo_offspring`` for DTLZ and LSMOP1, a warp-per-row pass over the children
+for LSMOP2-9).  DTLZ1-7 follow problems.py:69-136 op for op; results agree with
+NumPy to the last few ulps (transcendentals differ), inside the north star's 1e-5
+relative tolerance.  LSMOP1-9 are new (the reference has no LSMOP):
+the standard definitions of Cheng et al. 2017 in the PlatEMO formulation --
+linkage x^s_j <- (1 + j/D) x^s_j - 10 x_1 (LSMOP1-4) or (1 + cos(j/D pi/2)) x^s_j
+- 10 x_1 (LSMOP5-9), chaotic subcomponent sizes (c <- 3.8 c (1 - c), nk = 5),
+eta1 on odd / eta2 on even objectives (Sphere, Griewank, Schwefel 2.21, Rastrigin,
+Rosenbrock, Ackley per problem), and the linear (1-4), concave (5-8) or
+disconnected (9) front.  As in PlatEMO, the requested dimension only sizes the
 subcomponents; the problem then has D = m - 1 + nk * sum(sublen) variables
 (``make_problem("lsmop1", 3, 1000)`` has D = 992) and the linkage divides by
 that D.
@@ -25,7 +28,7 @@ from . import _lib
 from .directions import largest_h_for, simplex_lattice
 
 DTLZ = ("dtlz1", "dtlz2", "dtlz3", "dtlz4", "dtlz5", "dtlz6", "dtlz7")
-LSMOP = ("lsmop1",)
+LSMOP = tuple(f"lsmop{k}" for k in range(1, 10))
 _NAMES = DTLZ + LSMOP
 PROB_LSMOP1 = 101
 
@@ -111,7 +114,7 @@ class ProblemSpec:
         s = ProblemStruct()
         s.m, s.d = self.m, self.d
         if self.name in LSMOP:
-            s.id = PROB_LSMOP1
+            s.id = PROB_LSMOP1 + LSMOP.index(self.name)
             s.nk = 5
             sub, off = lsmop_groups_for(self.m, self.d, 5)
             for i in range(self.m):
@@ -179,8 +182,13 @@ def true_front(spec: ProblemSpec, count: int) -> np.ndarray:
     m = spec.m
     if spec.name in ("dtlz1",):
         return 0.5 * simplex_lattice(m, largest_h_for(count, m))
-    if spec.name in LSMOP:
+    if spec.name in ("lsmop1", "lsmop2", "lsmop3", "lsmop4"):  # linear front
         return simplex_lattice(m, largest_h_for(count, m))
+    if spec.name in ("lsmop5", "lsmop6", "lsmop7", "lsmop8"):  # concave front
+        pts = simplex_lattice(m, largest_h_for(count, m))
+        return pts / np.linalg.norm(pts, axis=1, keepdims=True)
+    if spec.name == "lsmop9":  # disconnected: f_M = 2 (M - sum f_k / 2 (1 + sin 3 pi f_k)), non-dominated
+        return _disconnected_front(m, count, 1.0)
     if spec.name in ("dtlz2", "dtlz3", "dtlz4"):
         pts = simplex_lattice(m, largest_h_for(count, m))
         return pts / np.linalg.norm(pts, axis=1, keepdims=True)
@@ -195,3 +203,23 @@ def true_front(spec: ProblemSpec, count: int) -> np.ndarray:
             out[:, i] = p
         return out
     raise ValueError(f"true_front not provided for {spec.name}")
+
+
+def _disconnected_front(m: int, count: int, G: float) -> np.ndarray:
+    """Non-dominated sample of the DTLZ7-type front f_M = (1 + G) (M - sum_k f_k / (1 + G) (1 + sin 3 pi f_k))
+    over a grid of the first m - 1 objectives (LSMOP9: G = 1 at the optimum)."""
+    per = max(2, int((max(count, 6000) + 0.5) ** (1.0 / max(m - 1, 1))))  # grid of <= ~6000 points
+    axes = np.meshgrid(*([np.linspace(0.0, 1.0, per)] * (m - 1)), indexing="ij")
+    pos = np.stack([a.reshape(-1) for a in axes], axis=1)
+    h = m - np.sum(pos / (1.0 + G) * (1.0 + np.sin(3.0 * np.pi * pos)), axis=1)
+    P = np.concatenate([pos, ((1.0 + G) * h)[:, None]], axis=1)
+    keep = np.ones(len(P), dtype=bool)
+    for a in range(0, len(P), 512):  # q dominates p: q <= p everywhere and q < p somewhere
+        blk = P[a: a + 512, None, :]
+        le = np.all(P[None, :, :] <= blk, axis=2)
+        lt = np.any(P[None, :, :] < blk, axis=2)
+        keep[a: a + 512] = ~np.any(le & lt, axis=1)
+    F = P[keep]
+    if len(F) > count:
+        F = F[np.linspace(0, len(F) - 1, count).astype(np.int64)]
+    return F

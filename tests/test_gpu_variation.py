@@ -113,7 +113,42 @@ def test_lsmop1_vs_self_oracle(cuda, m, d):
     assert np.allclose(evaluate(spec, X), oprob.evaluate_lsmop1(X, m), rtol=1e-12, atol=0)
 
 
-@pytest.mark.parametrize("name,m,d,n", [("dtlz1", 3, 12, 100), ("lsmop1", 3, 1000, 64), ("dtlz2", 5, 40, 33)])
+@pytest.mark.parametrize("k", range(2, 10))
+@pytest.mark.parametrize("m,d", [(3, 1000), (2, 300), (5, 700)])
+def test_lsmop_k_vs_self_oracle(cuda, k, m, d):
+    """LSMOP2-9 (warp-per-row kernel) vs the PlatEMO-form NumPy restatement."""
+    from paper_2503_20286_b200.problems import evaluate, make_problem
+
+    spec = make_problem(f"lsmop{k}", m=m, d=d)
+    d = spec.d
+    rng = np.random.default_rng(d + k)
+    X = spec.lower + rng.random((150, d)) * (spec.upper - spec.lower)
+    X[:5, m - 1:] = 10.0 * X[:5, :1] / (1.0 + np.arange(m, d + 1) / d)  # linkage-optimal rows (k <= 4)
+    want = oprob.evaluate_lsmop(k, X, m)
+    got = evaluate(spec, X)
+    assert np.allclose(got, want, rtol=1e-11, atol=1e-12 * np.abs(want).max())
+
+
+def test_evaluate_rows_map(cuda):
+    import torch
+
+    from paper_2503_20286_b200 import _lib
+    from paper_2503_20286_b200.problems import make_problem
+
+    for name in ("dtlz2", "lsmop1", "lsmop7"):
+        spec = make_problem(name, m=3, d=300 if name.startswith("lsmop") else 12)
+        X = torch.from_numpy(spec.lower + np.random.default_rng(3).random((64, spec.d)) * (spec.upper - spec.lower)).cuda()
+        rows = torch.from_numpy(np.random.default_rng(4).permutation(64)[:40].astype(np.int64)).cuda()
+        F = torch.empty((40, 3), dtype=torch.float64, device="cuda")
+        ps = spec.struct()
+        assert _lib.lib().temo_evaluate_rows(_lib.sptr(ps), _lib.ptr(X), _lib.ptr(rows), 40, _lib.ptr(F),
+                                             _lib.stream_handle(X.device)) == 0
+        want = oprob.evaluate(name, X[rows].cpu().numpy(), 3)
+        assert np.allclose(F.cpu().numpy(), want, rtol=1e-11, atol=0)
+
+
+@pytest.mark.parametrize("name,m,d,n", [("dtlz1", 3, 12, 100), ("lsmop1", 3, 1000, 64), ("dtlz2", 5, 40, 33),
+                                        ("lsmop3", 3, 1000, 64), ("lsmop9", 4, 400, 40)])
 def test_fused_offspring_matches_oracle(cuda, name, m, d, n):
     import torch
 
@@ -173,7 +208,8 @@ def test_sbx_beta_fast_vs_numpy(cuda):
 @pytest.mark.parametrize("name,m,d,h,pre", [("lsmop1", 3, 1000, 40, 0), ("lsmop1", 3, 1000, 40, 3),
                                             ("lsmop1", 3, 1000, 517, 1), ("lsmop1", 5, 700, 33, 2),
                                             ("dtlz1", 3, 12, 50, 1), ("dtlz2", 5, 40, 16, 2),
-                                            ("dtlz2", 3, 12, 1000, 3), ("dtlz7", 3, 13, 3, 0)])
+                                            ("dtlz2", 3, 12, 1000, 3), ("dtlz7", 3, 13, 3, 0),
+                                            ("lsmop6", 3, 1000, 40, 1), ("lsmop8", 5, 700, 33, 0)])
 def test_offspring_two_phase_equals_fused(cuda, name, m, d, h, pre):
     """temo_offspring_ws (randomness kernel + streaming apply kernel, the harness path) is
     bit-identical to the fused temo_offspring for every stream alignment (``pre`` shifts the

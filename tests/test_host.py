@@ -170,3 +170,54 @@ def test_run_config_fields_match_reference():
     with pytest.raises(ConfigError):
         RunConfig(algorithm="nsga3-seq").validate()
     RunConfig(algorithm="rvea").validate()
+
+
+def test_lsmop_family_known_answers():
+    """Self-oracle LSMOP1-9 (PlatEMO form): every eta vanishes at z = 0 except Rosenbrock
+    (L - 1 per subcomponent), so rows whose linkage maps x^s to 0 land on the linear (1-4),
+    concave (5-8) or disconnected (9) front, shifted by the Rosenbrock groups exactly."""
+    import math
+
+    from paper_2503_20286_b200.problems import LSMOP, make_problem
+
+    assert LSMOP == tuple(f"lsmop{k}" for k in range(1, 10))
+    m, nk = 3, 5
+    for k in range(1, 10):
+        spec = make_problem(f"lsmop{k}", m=m, d=300)
+        assert spec.struct().id == 100 + k
+        d = spec.d
+        sub, off = oprob.lsmop_groups_for(m, d)
+        pos = np.array([[0.3, 0.6], [0.0, 1.0], [0.9, 0.2]])
+        j = np.arange(m, d + 1) / d
+        c = np.cos(j * np.pi / 2.0) if k >= 5 else j
+        X = np.zeros((len(pos), d))
+        X[:, : m - 1] = pos
+        X[:, m - 1:] = 10.0 * pos[:, :1] / (1.0 + c)
+        F = oprob.evaluate_lsmop(k, X, m)
+        eta = oprob._ETA[k]
+        G = np.array([(nk * (sub[i] - 1) if eta[i % 2] == "rosenbrock" else 0.0) / sub[i] / nk for i in range(m)])
+        for r, p in enumerate(pos):
+            if k <= 4:
+                want = (1.0 + G) * np.array([p[0] * p[1], p[0] * (1 - p[1]), 1 - p[0]])
+            elif k <= 8:
+                a, b = p * math.pi / 2.0
+                Gn = np.append(G[1:], 0.0)
+                want = (1.0 + G + Gn) * np.array([math.cos(a) * math.cos(b), math.cos(a) * math.sin(b), math.sin(a)])
+            else:
+                gs = 1.0 + G.sum()
+                want = np.array([p[0], p[1], (1 + gs) * (m - np.sum(p / (1 + gs) * (1 + np.sin(3 * np.pi * p))))])
+            assert np.allclose(F[r], want, rtol=1e-9, atol=1e-9), (k, r, F[r], want)
+
+
+def test_lsmop_true_fronts():
+    from paper_2503_20286_b200.problems import make_problem, true_front
+
+    for k in range(1, 10):
+        F = true_front(make_problem(f"lsmop{k}", m=3, d=300), 200)
+        assert F.shape[1] == 3 and 3 <= len(F) <= 200
+        if k <= 4:
+            assert np.allclose(F.sum(axis=1), 1.0)
+        elif k <= 8:
+            assert np.allclose((F ** 2).sum(axis=1), 1.0)
+        else:
+            assert np.all(F[:, 2] >= 2.0 * 1.0)  # f_M = 2 (M - ...) >= 2 on the optimal front
