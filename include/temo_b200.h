@@ -412,6 +412,11 @@ int temo_neighbors(const double *W, int64_t r, int m, int T, int32_t *out, temo_
 double temo_probe_philox_rate(int blocks, int iters, uint64_t *scratch, temo_stream_t stream);
 double temo_probe_packed_rate(int blocks, int iters, uint64_t *scratch, temo_stream_t stream);
 double temo_probe_dsub_rate(int blocks, int iters, uint64_t *scratch, temo_stream_t stream);
+/* The offspring apply phase's access pattern alone (two gathered parent rows + one streamed
+ * row in, two scattered child rows out, per pair; d even): bytes/s over `iters` launches. */
+double temo_probe_rows_rate(const double *X, const int64_t *pa, const int64_t *pb, const double *B,
+                            const int64_t *dst, int64_t h, int64_t d, double *O, int iters,
+                            temo_stream_t stream);
 
 /* ------------------------------------------------------------ stage timing
  * CUDA-event timing of each kernel stage on its own stream (off by default).

@@ -101,6 +101,7 @@ SIGNATURES = {
     "temo_probe_philox_rate": (_D, [_I32, _I32, _P, _P]),
     "temo_probe_packed_rate": (_D, [_I32, _I32, _P, _P]),
     "temo_probe_dsub_rate": (_D, [_I32, _I32, _P, _P]),
+    "temo_probe_rows_rate": (_D, [_P, _P, _P, _P, _P, _I64, _I64, _P, _I32, _P]),
     "temo_timing_enable": (None, [_I32]),
     "temo_timing_name": (ctypes.c_char_p, [_I32]),
     "temo_timing_read": (_I32, [_P, _P, _I32]),

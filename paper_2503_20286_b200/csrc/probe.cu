@@ -90,6 +90,26 @@ __global__ void __launch_bounds__(256) k_probe_dsub(int iters, double seed, uint
     if (x == 1234.5) out[0] = 1;
 }
 
+// The apply phase's data movement alone: per pair q two gathered parent rows and one
+// streamed row in, two scattered child rows out (rows of d doubles, 16-byte vector accesses,
+// warp per pair) -- the achievable rate of k_offspring_apply's access pattern.
+__global__ void __launch_bounds__(256) k_probe_rows(const double2 *__restrict__ X, const int64_t *__restrict__ pa,
+                                                    const int64_t *__restrict__ pb, const double2 *__restrict__ B,
+                                                    const int64_t *__restrict__ dst, int64_t h, int64_t d2,
+                                                    double2 *__restrict__ O) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < h;
+         q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const double2 *x1 = X + pa[q] * d2, *x2 = X + pb[q] * d2, *bq = B + q * d2;
+        double2 *o1 = O + dst[q] * d2, *o2 = O + dst[h + q] * d2;
+        for (int64_t j = lane; j < d2; j += 32) {
+            const double2 a = x1[j], b = x2[j], c = bq[j];
+            o1[j] = make_double2(a.x + c.x * (b.x - a.x), a.y + c.y * (b.y - a.y));
+            o2[j] = make_double2(b.x + c.x * (a.x - b.x), b.y + c.y * (a.y - b.y));
+        }
+    }
+}
+
 }  // namespace temo
 
 namespace {
@@ -148,4 +168,35 @@ extern "C" double temo_probe_dsub_rate(int blocks, int iters, uint64_t *scratch,
     g_scratch = scratch;
     const double s = time_launches(launch_dsub, iters, (cudaStream_t)stream);
     return s > 0 ? (double)blocks * 256.0 * 8.0 * 16.0 * 2.0 * iters / s : -1.0;
+}
+
+// Bytes per second of k_probe_rows over h pairs of d-double rows (5 d doubles moved per pair);
+// X holds the parents (>= max(pa, pb) + 1 rows), O the children (>= max(dst) + 1 rows), B h rows.
+extern "C" double temo_probe_rows_rate(const double *X, const int64_t *pa, const int64_t *pb, const double *B,
+                                       const int64_t *dst, int64_t h, int64_t d, double *O, int iters,
+                                       temo_stream_t stream) {
+    if (!X || !pa || !pb || !B || !dst || !O || h < 1 || d < 2 || d % 2 || iters < 1) return -1.0;
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)(sms * 8);
+    auto launch = [&]() {
+        temo::k_probe_rows<<<grid, 256, 0, st>>>(reinterpret_cast<const double2 *>(X), pa, pb,
+                                                 reinterpret_cast<const double2 *>(B), dst, h, d / 2,
+                                                 reinterpret_cast<double2 *>(O));
+    };
+    launch();
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return -1.0;
+    cudaEventRecord(a, st);
+    for (int i = 0; i < iters; ++i) launch();
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (cudaGetLastError() != cudaSuccess || ms <= 0.f) return -1.0;
+    return 5.0 * 8.0 * (double)h * (double)d * iters / (ms * 1e-3);
 }

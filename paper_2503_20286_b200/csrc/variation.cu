@@ -629,6 +629,10 @@ __device__ void finish_objs(const temo_problem &P, const double *x, const double
     }
 }
 
+__device__ __forceinline__ uint64_t pick4u(const uint64_t v[4], int k) {
+    return k == 0 ? v[0] : k == 1 ? v[1] : k == 2 ? v[2] : v[3];
+}
+
 __device__ __forceinline__ double pick4(const double v[4], int k) {
     return k == 0 ? v[0] : k == 1 ? v[1] : k == 2 ? v[2] : v[3];
 }
@@ -1089,9 +1093,20 @@ __global__ void __launch_bounds__(SW * 32, OFF_S_MINB) k_offspring_s(temo_proble
 #ifndef OFF_APPLY_MINB
 #define OFF_APPLY_MINB 2
 #endif
+#ifndef OFF_APPLY_IDXPF
+#define OFF_APPLY_IDXPF 1
+#endif
+#ifndef OFF_APPLY_BQALL
+#define OFF_APPLY_BQALL 1
+#endif
+#ifndef OFF_APPLY_CSTORE
+#define OFF_APPLY_CSTORE 0
+#endif
 constexpr int RW = 8;  // warps per CTA of both phases
 
 __host__ __device__ inline int64_t quads_per_pair(int64_t d) { return (d + 3) / 4 + 1; }
+// per-pair stride of the flag rows: a multiple of 8 flags (16 bytes) so one pair's flags are one bulk copy
+__host__ __device__ inline int64_t flag_stride(int64_t d) { return (quads_per_pair(d) + 7) & ~(int64_t)7; }
 
 template <bool SWAP>
 __global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64_t d, VarArgs V, int64_t h,
@@ -1159,7 +1174,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64
                     if (!single) hit |= (uint32_t)(((okm >> k) & 1) && (int64_t)(R[1][k] >> 11) <= pm_thr) << (4 + k);
                 }
             }
-            if (j0 + lane < QP) flags[q * QP + j0 + lane] = (uint16_t)(crossed | hit << 4);
+            if (j0 + lane < QP) flags[q * flag_stride(d) + j0 + lane] = (uint16_t)(crossed | hit << 4);
             __syncwarp();
             for (int t = lane; t < total; t += 32) s_mu[warp][t] = sbx_beta(s_mu[warp][t], e);
             __syncwarp();
@@ -1198,7 +1213,8 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
     extern __shared__ double ssm[];
     const int64_t d = P.d;
     double *s_lo = ssm, *s_hi = ssm + d, *s_cf = ssm + 2 * d;
-    signed char *s_grp = reinterpret_cast<signed char *>(ssm + 3 * d);
+    double *s_wb = ssm + 3 * d;  // OFF_APPLY_CSTORE: RW x 2 x 128 doubles
+    signed char *s_grp = reinterpret_cast<signed char *>(ssm + 3 * d + (OFF_APPLY_CSTORE ? RW * 256 : 0));
     constexpr bool lsmop = LSMOP;
     for (int64_t g = threadIdx.x; g < d; g += blockDim.x) {
         s_lo[g] = V.lower[g];
@@ -1222,15 +1238,50 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
     const int64_t avail = 4 - ph.pos;
     const double eta = V.eta_m + 1.0;
     const int64_t QP = quads_per_pair(d);
-    for (int64_t q = q0 + (int64_t)blockIdx.x * RW + (threadIdx.x >> 5); q < q1; q += (int64_t)gridDim.x * RW) {
+    const int64_t qstride = (int64_t)gridDim.x * RW;
+#if OFF_APPLY_IDXPF
+    // index pipeline: pool rows of the next pair and raw parent indices of the one after are
+    // loaded while this pair streams (no dependent-load chain at the start of a pair)
+    int64_t qa = q0 + (int64_t)blockIdx.x * RW + (threadIdx.x >> 5);
+    auto prow = [&](const int64_t *ix, int64_t qq) { return src_map ? src_map[ix[qq]] : ix[qq]; };
+    auto drow = [&](int64_t r) { return dst_rows ? dst_rows[r] : r; };
+    int64_t np1 = 0, np2 = 0, nd1 = 0, nd2 = 0, nr1 = 0, nr2 = 0;
+    if (qa < q1) {
+        np1 = prow(i1, qa);
+        np2 = prow(i2, qa);
+        nd1 = drow(qa);
+        nd2 = drow(h + qa);
+    }
+    if (qa + qstride < q1) {
+        nr1 = i1[qa + qstride];
+        nr2 = i2[qa + qstride];
+    }
+#endif
+    for (int64_t q = q0 + (int64_t)blockIdx.x * RW + (threadIdx.x >> 5); q < q1; q += qstride) {
         // row pool (harness): parents at physical rows src_map[i], children into rows dst_rows[r]
+#if OFF_APPLY_IDXPF
+        const int64_t p1 = np1, p2 = np2;
+        double *o1 = O + nd1 * d;
+        double *o2 = O + nd2 * d;
+        if (q + qstride < q1) {
+            np1 = src_map ? src_map[nr1] : nr1;
+            np2 = src_map ? src_map[nr2] : nr2;
+            nd1 = drow(q + qstride);
+            nd2 = drow(h + q + qstride);
+        }
+        if (q + 2 * qstride < q1) {
+            nr1 = i1[q + 2 * qstride];
+            nr2 = i2[q + 2 * qstride];
+        }
+#else
         const int64_t p1 = src_map ? src_map[i1[q]] : i1[q];
         const int64_t p2 = src_map ? src_map[i2[q]] : i2[q];
+        double *o1 = O + (dst_rows ? dst_rows[q] : q) * d;
+        double *o2 = O + (dst_rows ? dst_rows[h + q] : h + q) * d;
+#endif
         const double *x1 = X + p1 * d;
         const double *x2 = X + p2 * d;
         const double *bq = beta + q * d;
-        double *o1 = O + (dst_rows ? dst_rows[q] : q) * d;
-        double *o2 = O + (dst_rows ? dst_rows[h + q] : h + q) * d;
         const int sh = (int)((o_mu + q * d - avail) & 3);
         double part1[M], part2[M];
 #pragma unroll
@@ -1249,7 +1300,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
                 }
             }
 #endif
-            const uint32_t fl = (j0 + lane < QP) ? flags[q * QP + j0 + lane] : 0u;
+            const uint32_t fl = (j0 + lane < QP) ? flags[q * flag_stride(d) + j0 + lane] : 0u;
             const uint32_t crossed = fl & 0xF, hit = (fl >> 4) & 0xFF;
             double c1[4], c2[4];
             bool ok[4];
@@ -1259,9 +1310,16 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
                 ok[k] = g >= 0 && g < d;
                 const double a = ok[k] ? __ldg(x1 + g) : 0.0;
                 const double b = ok[k] ? __ldg(x2 + g) : 0.0;
+#if OFF_APPLY_BQALL
+                const double bb = ok[k] ? __ldg(bq + g) : 0.0;  // same sectors either way: issue with a, b
+#endif
                 double y1 = a, y2 = b;
                 if ((crossed >> k) & 1) {
+#if OFF_APPLY_BQALL
+                    const double shift = 0.5 * (1.0 - bb);
+#else
                     const double shift = 0.5 * (1.0 - __ldg(bq + g));
+#endif
                     y1 = a + shift * (b - a);
                     y2 = b + shift * (a - b);
                 }
@@ -1285,12 +1343,34 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
                         c2[k] = clipv(pm_step(c2[k], s_lo[g], s_hi[g], u01(m2[k]), eta), s_lo[g], s_hi[g]);
                 }
             }
+#if OFF_APPLY_CSTORE
+            {  // children through a per-warp staging row: 256-byte coalesced stores (8 full sectors)
+                // instead of lane-strided quads (32 partial sectors per store instruction)
+                double *w1 = s_wb + (int64_t)(threadIdx.x >> 5) * 256, *w2 = w1 + 128;
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    w1[4 * lane + k] = c1[k];
+                    w2[4 * lane + k] = c2[k];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int64_t g = base + lane + 32 * i;
+                    if (g >= 0 && g < d) {
+                        o1[g] = w1[lane + 32 * i];
+                        if (!single) o2[g] = w2[lane + 32 * i];
+                    }
+                }
+            }
+#else
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (ok[k]) {
                     o1[gs + k] = c1[k];
                     if (!single) o2[gs + k] = c2[k];
                 }
+#endif
             if (!FO) continue;
             if (base == -sh) {
                 x0a = __shfl_sync(~0u, pick4(c1, sh), 0);
@@ -1337,6 +1417,668 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply(tem
 #pragma unroll
             for (int i = 0; i < M; ++i) FO[q * M + i] = f[i];
         } else if (lane == 1 && !single) {
+            double f[M];
+            finish_objs<M>(P, o2, part2, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[(h + q) * M + i] = f[i];
+        }
+    }
+}
+
+// ------------------------------------------------- apply phase, gene-major lanes (d >= 128)
+// k_offspring_apply with lane t owning genes 128 r + 32 k + t (k = 0..3) instead of the
+// Philox-aligned quad 4 t - sh: every global and shared access of the warp is a contiguous
+// 256-byte run (2 L1 wavefronts) instead of a 32-byte-strided one (8 wavefronts) -- the
+// quad kernel is L1-throughput bound (profiles/r02_ncu_D_offspring_apply_quad.txt: l1tex
+// 62-73 % of peak, DRAM 36 %).  A gene's flag bits come from its stream quad
+// (g + sh) >> 2 by warp shuffle; PM's rare draws use the same aligned Philox block.
+// Children are bit-identical to the quad kernels; the objective sums run in another order.
+template <int M, bool LSMOP>
+__global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply_t(temo_problem P, VarArgs V,
+                                                                  const double *__restrict__ X,
+                                                                  const int64_t *__restrict__ i1,
+                                                                  const int64_t *__restrict__ i2, int64_t h,
+                                                                  int64_t q0, int64_t q1,
+                                                                  Philox ph, uint64_t off, int swap,
+                                                                  const double *__restrict__ beta,
+                                                                  const uint16_t *__restrict__ flags,
+                                                                  double *__restrict__ O,
+                                                                  double *__restrict__ FO,
+                                                                  const int64_t *__restrict__ src_map,
+                                                                  const int64_t *__restrict__ dst_rows) {
+    extern __shared__ double tsm[];
+    const int64_t d = P.d;
+    double *s_lo = tsm, *s_hi = tsm + d, *s_cf = tsm + 2 * d;
+    signed char *s_grp = reinterpret_cast<signed char *>(tsm + 3 * d);
+    for (int64_t g = threadIdx.x; g < d; g += blockDim.x) {
+        s_lo[g] = V.lower[g];
+        s_hi[g] = V.upper[g];
+        s_cf[g] = 1.0 + (double)(g + 1) / (double)d;
+        int grp = -1;
+        const int64_t rel = g - (M - 1);
+        if (LSMOP) {
+            for (int i = 0; i < M; ++i)
+                if (rel >= P.offset[i] && rel < P.offset[i + 1]) grp = i;
+        } else if (rel >= 0) {
+            grp = 0;
+        }
+        s_grp[g] = (signed char)grp;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t hd = h * d;
+    const int64_t o_mu = (int64_t)off;
+    const int64_t o_pmu = o_mu + (swap ? 3 * hd : hd);
+    const int64_t avail = 4 - ph.pos;
+    const double eta = V.eta_m + 1.0;
+    const int64_t QP = quads_per_pair(d), QS = flag_stride(d);
+    const int64_t qstride = (int64_t)gridDim.x * RW;
+    const int64_t qa = q0 + (int64_t)blockIdx.x * RW + (threadIdx.x >> 5);
+    auto prow = [&](const int64_t *ix, int64_t qq) { return src_map ? src_map[ix[qq]] : ix[qq]; };
+    auto drow = [&](int64_t r) { return dst_rows ? dst_rows[r] : r; };
+    int64_t np1 = 0, np2 = 0, nd1 = 0, nd2 = 0, nr1 = 0, nr2 = 0;  // index pipeline (next pairs)
+    if (qa < q1) {
+        np1 = prow(i1, qa);
+        np2 = prow(i2, qa);
+        nd1 = drow(qa);
+        nd2 = drow(h + qa);
+    }
+    if (qa + qstride < q1) {
+        nr1 = i1[qa + qstride];
+        nr2 = i2[qa + qstride];
+    }
+    for (int64_t q = qa; q < q1; q += qstride) {
+        const double *x1 = X + np1 * d;
+        const double *x2 = X + np2 * d;
+        double *o1 = O + nd1 * d;
+        double *o2 = O + nd2 * d;
+        if (q + qstride < q1) {
+            np1 = src_map ? src_map[nr1] : nr1;
+            np2 = src_map ? src_map[nr2] : nr2;
+            nd1 = drow(q + qstride);
+            nd2 = drow(h + q + qstride);
+        }
+        if (q + 2 * qstride < q1) {
+            nr1 = i1[q + 2 * qstride];
+            nr2 = i2[q + 2 * qstride];
+        }
+        const double *bq = beta + q * d;
+        const uint16_t *fq = flags + q * QS;
+        const int sh = (int)((o_mu + q * d - avail) & 3);
+        const int bit = (lane + sh) & 3;        // position of this lane's genes in their stream quads
+        const int jl = (lane + sh) >> 2;        // quad of gene (32 k + lane) is 8 k + jl within the round
+        double part1[M], part2[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) part1[i] = part2[i] = 0.0;
+        double x0a = 0.0, x0b = 0.0;
+        for (int64_t base = 0, j0 = 0; base < d; base += 128, j0 += 32) {
+            const uint32_t fa = (j0 + lane < QP) ? fq[j0 + lane] : 0u;
+            const uint32_t fb = (j0 + 32 < QP) ? fq[j0 + 32] : 0u;
+            double a[4], b[4], bb[4];
+            bool ok[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t g = base + 32 * k + lane;
+                ok[k] = g < d;
+                a[k] = ok[k] ? __ldg(x1 + g) : 0.0;
+                b[k] = ok[k] ? __ldg(x2 + g) : 0.0;
+                bb[k] = ok[k] ? __ldg(bq + g) : 0.0;
+            }
+            double c1[4], c2[4];
+            uint32_t hit = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int src = 8 * k + jl;  // <= 32
+                const uint32_t w0 = __shfl_sync(~0u, fa, src & 31);
+                const uint32_t w = src < 32 ? w0 : fb;
+                const int64_t g = base + 32 * k + lane;
+                double y1 = a[k], y2 = b[k];
+                if ((w >> bit) & 1) {
+                    const double shift = 0.5 * (1.0 - bb[k]);
+                    y1 = a[k] + shift * (b[k] - a[k]);
+                    y2 = b[k] + shift * (a[k] - b[k]);
+                }
+                if (ok[k]) {
+                    y1 = clipv(y1, s_lo[g], s_hi[g]);
+                    y2 = clipv(y2, s_lo[g], s_hi[g]);
+                    hit |= ((w >> (4 + bit)) & 1u) << k;
+                    hit |= ((w >> (8 + bit)) & 1u) << (4 + k);
+                }
+                c1[k] = y1;
+                c2[k] = y2;
+            }
+            if (hit) {  // polynomial mutation (variation.py:104-120), only where hit
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (!((hit >> k) & 0x11)) continue;
+                    const int64_t g = base + 32 * k + lane;
+                    const int64_t es = q * d + g - bit;  // start of the gene's stream quad
+                    if ((hit >> k) & 1) {
+                        uint64_t m[4];
+                        raw_quad(ph, o_pmu + es, avail, m);
+                        c1[k] = clipv(pm_step(c1[k], s_lo[g], s_hi[g], u01(pick4u(m, bit)), eta), s_lo[g], s_hi[g]);
+                    }
+                    if ((hit >> (4 + k)) & 1) {
+                        uint64_t m[4];
+                        raw_quad(ph, o_pmu + hd + es, avail, m);
+                        c2[k] = clipv(pm_step(c2[k], s_lo[g], s_hi[g], u01(pick4u(m, bit)), eta), s_lo[g], s_hi[g]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (ok[k]) {
+                    o1[base + 32 * k + lane] = c1[k];
+                    o2[base + 32 * k + lane] = c2[k];
+                }
+            if (!FO) continue;
+            if (base == 0) {
+                x0a = __shfl_sync(~0u, c1[0], 0);
+                x0b = __shfl_sync(~0u, c2[0], 0);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!ok[k]) continue;
+                const int64_t g = base + 32 * k + lane;
+                if constexpr (LSMOP) {
+                    const int grp = (int)s_grp[g];
+                    if (grp < 0) continue;
+                    const double cf = s_cf[g];
+                    const double xa = cf * c1[k] - 10.0 * x0a;
+                    const double xb = cf * c2[k] - 10.0 * x0b;
+#pragma unroll
+                    for (int i = 0; i < M; ++i)
+                        if (grp == i) {
+                            part1[i] += xa * xa;
+                            part2[i] += xb * xb;
+                        }
+                } else {
+                    acc_gene<M>(P, g, c1[k], x0a, part1);
+                    acc_gene<M>(P, g, c2[k], x0b, part2);
+                }
+            }
+        }
+        if (!FO) continue;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int s = 16; s; s >>= 1) {
+                part1[i] += __shfl_xor_sync(~0u, part1[i], s);
+                part2[i] += __shfl_xor_sync(~0u, part2[i], s);
+            }
+        __syncwarp();
+        if (lane == 0) {
+            double f[M];
+            finish_objs<M>(P, o1, part1, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[q * M + i] = f[i];
+        } else if (lane == 1) {
+            double f[M];
+            finish_objs<M>(P, o2, part2, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[(h + q) * M + i] = f[i];
+        }
+    }
+}
+
+// ------------------------------------------------- apply phase, vector gene-major (d even)
+// The apply phase's data movement runs at 6.2 TB/s as a plain warp-per-pair double2 stream
+// (temo_probe_rows_rate: two gathered rows + one streamed row in, two scattered rows out) --
+// at 64 warps/SM.  This kernel keeps that shape: lane t owns genes 64 s + 2 t + {0, 1}
+// (16-byte loads and stores, every warp access one contiguous 512-byte run), registers are
+// capped for 4 CTAs/SM, a gene's flag bits come from its stream quad (g + sh) >> 2 by warp
+// shuffle and PM's rare draws from the same aligned Philox block (out of line).  Children are
+// bit-identical to the quad kernels; the objective sums run in another order.  Measured at
+// pop 200k (ms): quad kernel 1.41; this kernel 1.22 (3 CTAs/SM, PM out of line), 1.26 (4 CTAs/SM,
+// spills), 1.36 / 1.28 with PM inlined (3 / 4 CTAs/SM); scalar gene-major 1.68; per-warp bulk
+// ring 1.66; CTA-per-pair bulk stages 1.86; coalesced-store staging 1.48.
+#ifndef OFF_APPLYV_MINB
+#define OFF_APPLYV_MINB 3
+#endif
+static __device__ __noinline__ double pm_gene(const Philox &ph, int64_t e_quad, int64_t avail, int bit, double c,
+                                              double lo, double hi, double eta) {
+    uint64_t m[4];
+    raw_quad(ph, e_quad, avail, m);
+    return clipv(pm_step(c, lo, hi, u01(pick4u(m, bit)), eta), lo, hi);
+}
+
+template <int M, bool LSMOP>
+__global__ void __launch_bounds__(RW * 32, OFF_APPLYV_MINB) k_offspring_apply_v(temo_problem P, VarArgs V,
+                                                                   const double *__restrict__ X,
+                                                                   const int64_t *__restrict__ i1,
+                                                                   const int64_t *__restrict__ i2, int64_t h,
+                                                                   int64_t q0, int64_t q1,
+                                                                   const __grid_constant__ Philox ph, uint64_t off, int swap,
+                                                                   const double *__restrict__ beta,
+                                                                   const uint16_t *__restrict__ flags,
+                                                                   double *__restrict__ O,
+                                                                   double *__restrict__ FO,
+                                                                   const int64_t *__restrict__ src_map,
+                                                                   const int64_t *__restrict__ dst_rows) {
+    extern __shared__ __align__(16) double vsm[];
+    const int64_t d = P.d;
+    double *s_lo = vsm, *s_hi = vsm + d, *s_cf = vsm + 2 * d;
+    signed char *s_grp = reinterpret_cast<signed char *>(vsm + 3 * d);
+    for (int64_t g = threadIdx.x; g < d; g += blockDim.x) {
+        s_lo[g] = V.lower[g];
+        s_hi[g] = V.upper[g];
+        s_cf[g] = 1.0 + (double)(g + 1) / (double)d;
+        int grp = -1;
+        const int64_t rel = g - (M - 1);
+        if (LSMOP) {
+            for (int i = 0; i < M; ++i)
+                if (rel >= P.offset[i] && rel < P.offset[i + 1]) grp = i;
+        } else if (rel >= 0) {
+            grp = 0;
+        }
+        s_grp[g] = (signed char)grp;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t hd = h * d;
+    const int64_t o_mu = (int64_t)off;
+    const int64_t o_pmu = o_mu + (swap ? 3 * hd : hd);
+    const int64_t avail = 4 - ph.pos;
+    const double eta = V.eta_m + 1.0;
+    const int64_t QP = quads_per_pair(d), QS = flag_stride(d);
+    const int64_t d2 = d >> 1;
+    for (int64_t q = q0 + (int64_t)blockIdx.x * RW + (threadIdx.x >> 5); q < q1; q += (int64_t)gridDim.x * RW) {
+        const int64_t p1 = src_map ? src_map[i1[q]] : i1[q];
+        const int64_t p2 = src_map ? src_map[i2[q]] : i2[q];
+        const double2 *x1 = reinterpret_cast<const double2 *>(X + p1 * d);
+        const double2 *x2 = reinterpret_cast<const double2 *>(X + p2 * d);
+        const double2 *bq = reinterpret_cast<const double2 *>(beta + q * d);
+        double2 *o1 = reinterpret_cast<double2 *>(O + (dst_rows ? dst_rows[q] : q) * d);
+        double2 *o2 = reinterpret_cast<double2 *>(O + (dst_rows ? dst_rows[h + q] : h + q) * d);
+        const uint16_t *fq = flags + q * QS;
+        const int sh = (int)((o_mu + q * d - avail) & 3);
+        double part1[M], part2[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) part1[i] = part2[i] = 0.0;
+        double x0a = 0.0, x0b = 0.0;
+        for (int64_t v0 = 0; v0 < d2; v0 += 32) {  // 64 genes per round: lane owns pair v = v0 + lane
+            const int64_t v = v0 + lane;
+            const bool ok = v < d2;
+            const int64_t jq = (2 * v0) >> 2;           // first stream quad of the round (v0 % 32 == 0)
+            const uint32_t fw = (lane <= 16 && jq + lane < QP) ? fq[jq + lane] : 0u;
+            const double2 a = ok ? __ldg(x1 + v) : make_double2(0.0, 0.0);
+            const double2 b = ok ? __ldg(x2 + v) : make_double2(0.0, 0.0);
+            const double2 bb = ok ? __ldg(bq + v) : make_double2(0.0, 0.0);
+            const int g0 = 2 * lane + sh;                 // round-relative stream position of gene 2v
+            const uint32_t w0 = __shfl_sync(~0u, fw, g0 >> 2), w1 = __shfl_sync(~0u, fw, (g0 + 1) >> 2);
+            const int b0 = g0 & 3, b1 = (g0 + 1) & 3;
+            double y[2][2];
+            const double av[2] = {a.x, a.y}, bv[2] = {b.x, b.y}, sv[2] = {bb.x, bb.y};
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t w = e ? w1 : w0;
+                const int bit = e ? b1 : b0;
+                double y1 = av[e], y2 = bv[e];
+                if ((w >> bit) & 1) {
+                    const double shift = 0.5 * (1.0 - sv[e]);
+                    y1 = av[e] + shift * (bv[e] - av[e]);
+                    y2 = bv[e] + shift * (av[e] - bv[e]);
+                }
+                const int64_t g = 2 * v + e;
+                if (ok) {
+                    const double lo = s_lo[g], hi = s_hi[g];
+                    y1 = clipv(y1, lo, hi);
+                    y2 = clipv(y2, lo, hi);
+                    const int64_t eq = q * d + g - bit;  // start of the gene's stream quad
+                    if ((w >> (4 + bit)) & 1) y1 = pm_gene(ph, o_pmu + eq, avail, bit, y1, lo, hi, eta);
+                    if ((w >> (8 + bit)) & 1) y2 = pm_gene(ph, o_pmu + hd + eq, avail, bit, y2, lo, hi, eta);
+                }
+                y[0][e] = y1;
+                y[1][e] = y2;
+            }
+            if (ok) {
+                o1[v] = make_double2(y[0][0], y[0][1]);
+                o2[v] = make_double2(y[1][0], y[1][1]);
+            }
+            if (!FO) continue;
+            if (v0 == 0) {
+                x0a = __shfl_sync(~0u, y[0][0], 0);
+                x0b = __shfl_sync(~0u, y[1][0], 0);
+            }
+            if (!ok) continue;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int64_t g = 2 * v + e;
+                if constexpr (LSMOP) {
+                    const int grp = (int)s_grp[g];
+                    if (grp < 0) continue;
+                    const double cf = s_cf[g];
+                    const double xa = cf * y[0][e] - 10.0 * x0a;
+                    const double xb = cf * y[1][e] - 10.0 * x0b;
+#pragma unroll
+                    for (int i = 0; i < M; ++i)
+                        if (grp == i) {
+                            part1[i] += xa * xa;
+                            part2[i] += xb * xb;
+                        }
+                } else {
+                    acc_gene<M>(P, g, y[0][e], x0a, part1);
+                    acc_gene<M>(P, g, y[1][e], x0b, part2);
+                }
+            }
+        }
+        if (!FO) continue;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int s = 16; s; s >>= 1) {
+                part1[i] += __shfl_xor_sync(~0u, part1[i], s);
+                part2[i] += __shfl_xor_sync(~0u, part2[i], s);
+            }
+        __syncwarp();
+        if (lane == 0) {
+            double f[M];
+            finish_objs<M>(P, reinterpret_cast<const double *>(o1), part1, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[q * M + i] = f[i];
+        } else if (lane == 1) {
+            double f[M];
+            finish_objs<M>(P, reinterpret_cast<const double *>(o2), part2, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[(h + q) * M + i] = f[i];
+        }
+    }
+}
+
+// ------------------------------------------------- apply phase, per-warp bulk ring (d even)
+// k_offspring_apply with its loads moved off the critical path: each warp keeps a ring of
+// OFF_RING_S stages in shared memory, and its lane 0 streams the next rounds' parent-row,
+// spread-factor and flag chunks (<= 130 + 130 + 130 doubles + 32 flags per round) into it
+// with cp.async.bulk on a per-stage mbarrier, crossing pair boundaries (the pool rows of the
+// next pair are looked up one pair ahead).  Up to OFF_RING_S rounds per warp are in flight
+// while it computes, instead of one.  Gene quads, lanes, rounds and the summation order are
+// those of k_offspring_apply, so children and objectives are bit-identical to it.
+// (A CTA-per-pair variant with whole-row bulk stages measured 1.86 ms vs 1.44 ms at pop 200k,
+// barrier-bound: profiles/r02_ncu_D_offspring_apply_bulk.txt.)
+#ifndef OFF_RING_S
+#define OFF_RING_S 3
+#endif
+constexpr int RING_CH = 130;                        // doubles per row chunk (128 genes + alignment)
+constexpr int RING_STAGE = 3 * RING_CH + 8;         // doubles per stage: x1, x2, beta chunks + 32 flags
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+
+template <int M, bool LSMOP>
+__global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply_ring(temo_problem P, VarArgs V,
+                                                                     const double *__restrict__ X,
+                                                                     const int64_t *__restrict__ i1,
+                                                                     const int64_t *__restrict__ i2, int64_t h,
+                                                                     int64_t q0, int64_t q1,
+                                                                     Philox ph, uint64_t off, int swap,
+                                                                     const double *__restrict__ beta,
+                                                                     const uint16_t *__restrict__ flags,
+                                                                     double *__restrict__ O,
+                                                                     double *__restrict__ FO,
+                                                                     const int64_t *__restrict__ src_map,
+                                                                     const int64_t *__restrict__ dst_rows) {
+    constexpr int RS = OFF_RING_S;
+    extern __shared__ __align__(16) double rsm[];
+    const int64_t d = P.d;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *ring = rsm + (int64_t)warp * RS * RING_STAGE;                     // this warp's stages
+    uint64_t *bar = reinterpret_cast<uint64_t *>(rsm + (int64_t)RW * RS * RING_STAGE) + warp * RS;
+    double *s_lo = rsm + (int64_t)RW * RS * RING_STAGE + RW * RS, *s_hi = s_lo + d, *s_cf = s_hi + d;
+    double *s_wb = s_cf + d;  // OFF_APPLY_CSTORE staging rows
+    signed char *s_grp = reinterpret_cast<signed char *>(s_cf + d + (OFF_APPLY_CSTORE ? RW * 256 : 0));
+    for (int64_t g = threadIdx.x; g < d; g += blockDim.x) {
+        s_lo[g] = V.lower[g];
+        s_hi[g] = V.upper[g];
+        s_cf[g] = 1.0 + (double)(g + 1) / (double)d;
+        int grp = -1;
+        const int64_t rel = g - (M - 1);
+        if (LSMOP) {
+            for (int i = 0; i < M; ++i)
+                if (rel >= P.offset[i] && rel < P.offset[i + 1]) grp = i;
+        } else if (rel >= 0) {
+            grp = 0;
+        }
+        s_grp[g] = (signed char)grp;
+    }
+    if (lane == 0) {
+        for (int st = 0; st < RS; ++st) mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t hd = h * d;
+    const int64_t o_mu = (int64_t)off;
+    const int64_t o_pmu = o_mu + (swap ? 3 * hd : hd);
+    const int64_t avail = 4 - ph.pos;
+    const double eta = V.eta_m + 1.0;
+    const int64_t QP = quads_per_pair(d), QS = flag_stride(d);
+    const int64_t qstride = (int64_t)gridDim.x * RW;
+    const int64_t qa = q0 + (int64_t)blockIdx.x * RW + warp;
+    auto shift_of = [&](int64_t q) { return (int)((o_mu + q * d - avail) & 3); };
+    auto rounds_of = [&](int sh) { return (d + sh + 127) / 128; };
+    auto mapped = [&](int64_t r) { return src_map ? src_map[r] : r; };
+    auto drow = [&](int64_t r) { return dst_rows ? dst_rows[r] : r; };
+    // producer cursor (uniform over the warp; lane 0 issues): pair pq, round pr of pR, rows pp1/pp2
+    int64_t pq = qa, pr = 0, pR = 0, pp1 = 0, pp2 = 0, np1 = 0, np2 = 0, nr1 = 0, nr2 = 0;
+    int psh = 0;
+    if (pq < q1) {
+        pp1 = mapped(i1[pq]);
+        pp2 = mapped(i2[pq]);
+        psh = shift_of(pq);
+        pR = rounds_of(psh);
+        if (pq + qstride < q1) {
+            np1 = mapped(i1[pq + qstride]);
+            np2 = mapped(i2[pq + qstride]);
+        }
+        if (pq + 2 * qstride < q1) {
+            nr1 = i1[pq + 2 * qstride];
+            nr2 = i2[pq + 2 * qstride];
+        }
+    }
+    int64_t issued = 0;
+    auto issue_next = [&]() {
+        if (pq >= q1) return;
+        const int st = (int)(issued % RS);
+        if (lane == 0) {
+            const int64_t b = -psh + 128 * pr;
+            const int64_t lo = (b < 0 ? 0 : b) & ~(int64_t)1;
+            const int64_t hi = ((b + 128 < d ? b + 128 : d) + 1) & ~(int64_t)1;
+            const uint32_t nb = (uint32_t)((hi - lo) * sizeof(double));
+            const int64_t f0 = 32 * pr, fn = (QS - f0 < 32 ? QS - f0 : 32);
+            const uint32_t fb = (uint32_t)(fn * sizeof(uint16_t));
+            double *dst = ring + (int64_t)st * RING_STAGE;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bar[st], 3 * nb + fb);
+            bulk_g2s(dst, X + pp1 * d + lo, nb, &bar[st]);
+            bulk_g2s(dst + RING_CH, X + pp2 * d + lo, nb, &bar[st]);
+            bulk_g2s(dst + 2 * RING_CH, beta + pq * d + lo, nb, &bar[st]);
+            bulk_g2s(dst + 3 * RING_CH, flags + pq * QS + f0, fb, &bar[st]);
+        }
+        ++issued;
+        if (++pr == pR) {  // next pair of this warp
+            pq += qstride;
+            pr = 0;
+            if (pq < q1) {
+                pp1 = np1;
+                pp2 = np2;
+                psh = shift_of(pq);
+                pR = rounds_of(psh);
+                if (pq + qstride < q1) {
+                    np1 = mapped(nr1);
+                    np2 = mapped(nr2);
+                }
+                if (pq + 2 * qstride < q1) {
+                    nr1 = i1[pq + 2 * qstride];
+                    nr2 = i2[pq + 2 * qstride];
+                }
+            }
+        }
+    };
+    for (int k = 0; k < RS; ++k) issue_next();
+    int64_t used = 0;
+    int64_t nd1 = 0, nd2 = 0;
+    if (qa < q1) {
+        nd1 = drow(qa);
+        nd2 = drow(h + qa);
+    }
+    for (int64_t q = qa; q < q1; q += qstride) {
+        double *o1 = O + nd1 * d;
+        double *o2 = O + nd2 * d;
+        if (q + qstride < q1) {
+            nd1 = drow(q + qstride);
+            nd2 = drow(h + q + qstride);
+        }
+        const int sh = shift_of(q);
+        double part1[M], part2[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) part1[i] = part2[i] = 0.0;
+        double x0a = 0.0, x0b = 0.0;
+        for (int64_t base = -sh, j0 = 0; base < d; base += 128, j0 += 32) {
+            const int st = (int)(used % RS);
+            mbar_wait(&bar[st], (uint32_t)((used / RS) & 1));
+            const double *cx1 = ring + (int64_t)st * RING_STAGE;
+            const double *cx2 = cx1 + RING_CH, *cbq = cx2 + RING_CH;
+            const uint16_t *cfl = reinterpret_cast<const uint16_t *>(cbq + RING_CH);
+            const int64_t lo = (base < 0 ? 0 : base) & ~(int64_t)1;
+            const int64_t gs = base + 4 * lane;
+            const int64_t es = q * d + gs;
+            const uint32_t fl = (j0 + lane < QP) ? cfl[lane] : 0u;
+            const uint32_t crossed = fl & 0xF, hit = (fl >> 4) & 0xFF;
+            double c1[4], c2[4];
+            bool ok[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t g = gs + k;
+                ok[k] = g >= 0 && g < d;
+                const double a = ok[k] ? cx1[g - lo] : 0.0;
+                const double b = ok[k] ? cx2[g - lo] : 0.0;
+                const double bb = ok[k] ? cbq[g - lo] : 0.0;
+                double y1 = a, y2 = b;
+                if ((crossed >> k) & 1) {
+                    const double shift = 0.5 * (1.0 - bb);
+                    y1 = a + shift * (b - a);
+                    y2 = b + shift * (a - b);
+                }
+                if (ok[k]) {
+                    y1 = clipv(y1, s_lo[g], s_hi[g]);
+                    y2 = clipv(y2, s_lo[g], s_hi[g]);
+                }
+                c1[k] = y1;
+                c2[k] = y2;
+            }
+            __syncwarp();  // stage consumed by every lane: refill it with the round RS ahead
+            ++used;
+            issue_next();
+            if (hit) {  // polynomial mutation (variation.py:104-120), only where hit
+                uint64_t m1[4], m2[4];
+                if (hit & 0xF) raw_quad(ph, o_pmu + es, avail, m1);
+                if (hit & 0xF0) raw_quad(ph, o_pmu + hd + es, avail, m2);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t g = gs + k;
+                    if ((hit >> k) & 1)
+                        c1[k] = clipv(pm_step(c1[k], s_lo[g], s_hi[g], u01(m1[k]), eta), s_lo[g], s_hi[g]);
+                    if ((hit >> (4 + k)) & 1)
+                        c2[k] = clipv(pm_step(c2[k], s_lo[g], s_hi[g], u01(m2[k]), eta), s_lo[g], s_hi[g]);
+                }
+            }
+#if OFF_APPLY_CSTORE
+            {
+                double *w1 = s_wb + (int64_t)warp * 256, *w2 = w1 + 128;
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    w1[4 * lane + k] = c1[k];
+                    w2[4 * lane + k] = c2[k];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int64_t g = base + lane + 32 * i;
+                    if (g >= 0 && g < d) {
+                        o1[g] = w1[lane + 32 * i];
+                        o2[g] = w2[lane + 32 * i];
+                    }
+                }
+            }
+#else
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (ok[k]) {
+                    o1[gs + k] = c1[k];
+                    o2[gs + k] = c2[k];
+                }
+#endif
+            if (!FO) continue;
+            if (base == -sh) {
+                x0a = __shfl_sync(~0u, pick4(c1, sh), 0);
+                x0b = __shfl_sync(~0u, pick4(c2, sh), 0);
+            }
+            if constexpr (LSMOP) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int grp = ok[k] ? (int)s_grp[gs + k] : -1;
+                    if (grp < 0) continue;
+                    const double cf = s_cf[gs + k];
+                    const double xa = cf * c1[k] - 10.0 * x0a;
+                    const double sa = xa * xa;
+                    const double xb = cf * c2[k] - 10.0 * x0b;
+                    const double sb = xb * xb;
+#pragma unroll
+                    for (int i = 0; i < M; ++i)
+                        if (grp == i) {
+                            part1[i] += sa;
+                            part2[i] += sb;
+                        }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (ok[k]) {
+                        acc_gene<M>(P, gs + k, c1[k], x0a, part1);
+                        acc_gene<M>(P, gs + k, c2[k], x0b, part2);
+                    }
+            }
+        }
+        if (!FO) continue;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int s = 16; s; s >>= 1) {
+                part1[i] += __shfl_xor_sync(~0u, part1[i], s);
+                part2[i] += __shfl_xor_sync(~0u, part2[i], s);
+            }
+        __syncwarp();
+        if (lane == 0) {
+            double f[M];
+            finish_objs<M>(P, o1, part1, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) FO[q * M + i] = f[i];
+        } else if (lane == 1) {
             double f[M];
             finish_objs<M>(P, o2, part2, f);
 #pragma unroll
@@ -1407,6 +2149,36 @@ static bool offspring_s_disabled() {
     if (v < 0) {
         const char *e = getenv("TEMO_OFFSPRING_S");
         v = (e && e[0] == '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+// TEMO_APPLY_VEC=0 disables the vector gene-major apply kernel (d even, >= 128) (A/B)
+static bool apply_vec() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_APPLY_VEC");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// TEMO_APPLY_GENE=1 selects the scalar gene-major apply kernel for d >= 128 (A/B; slower)
+static bool apply_gene_major() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_APPLY_GENE");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+// TEMO_APPLY_RING=1 selects the bulk-ring apply kernel instead of the plain warp-per-pair one (A/B)
+static bool apply_ring_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_APPLY_RING");
+        v = (e && e[0] == '1') ? 1 : 0;
     }
     return v == 1;
 }
@@ -1513,6 +2285,53 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
             const double *beta, const uint16_t *flags, double *O, double *FO,
             const int64_t *src_map, const int64_t *dst_rows, size_t sm_a, unsigned grid,
             cudaStream_t s) {
+    const int64_t d = prob->d;
+    if (d >= 128 && d % 2 == 0 && apply_vec()) {
+        const size_t sm_v = 3 * d * sizeof(double) + d + 16;
+        if (sm_v > 48 * 1024) {
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply_v<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply_v<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
+        }
+        const int64_t want = (q1 - q0 + RW - 1) / RW;
+        const unsigned gv = (unsigned)(want < num_sms() * OFF_APPLYV_MINB * 8 ? want : num_sms() * OFF_APPLYV_MINB * 8);
+        if (prob->id == TEMO_PROB_LSMOP1)
+            k_offspring_apply_v<M, true><<<gv, RW * 32, sm_v, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
+                                                                gene_swap, beta, flags, O, FO, src_map, dst_rows);
+        else
+            k_offspring_apply_v<M, false><<<gv, RW * 32, sm_v, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
+                                                                 gene_swap, beta, flags, O, FO, src_map, dst_rows);
+        return TEMO_OK;
+    }
+    if (d >= 128 && apply_gene_major()) {
+        const size_t sm_t = 3 * d * sizeof(double) + d + 16;
+        if (sm_t > 48 * 1024) {
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply_t<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_t));
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply_t<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_t));
+        }
+        if (prob->id == TEMO_PROB_LSMOP1)
+            k_offspring_apply_t<M, true><<<grid, RW * 32, sm_t, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
+                                                                  gene_swap, beta, flags, O, FO, src_map, dst_rows);
+        else
+            k_offspring_apply_t<M, false><<<grid, RW * 32, sm_t, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
+                                                                   gene_swap, beta, flags, O, FO, src_map, dst_rows);
+        return TEMO_OK;
+    }
+    if (d % 2 == 0 && d >= 128 && apply_ring_enabled()) {  // per-warp bulk ring (rows 16-byte aligned)
+        const size_t sm_r = (size_t)RW * OFF_RING_S * (RING_STAGE * sizeof(double) + sizeof(uint64_t)) + sm_a;
+        if (sm_r <= 227 * 1024) {
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply_ring<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_r));
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply_ring<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_r));
+            if (prob->id == TEMO_PROB_LSMOP1)
+                k_offspring_apply_ring<M, true><<<grid, RW * 32, sm_r, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
+                                                                         gene_swap, beta, flags, O, FO, src_map,
+                                                                         dst_rows);
+            else
+                k_offspring_apply_ring<M, false><<<grid, RW * 32, sm_r, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph,
+                                                                          off, gene_swap, beta, flags, O, FO,
+                                                                          src_map, dst_rows);
+            return TEMO_OK;
+        }
+    }
     if (sm_a > 48 * 1024) {
         TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a));
         TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_a));
@@ -1680,7 +2499,7 @@ static int launch_offspring(const temo_problem *prob, const temo_variation *var,
 extern "C" size_t temo_offspring_ws_bytes(int64_t h, int64_t d) {
     if (h < 0 || d < 1) return 0;
     return (size_t)round_up((int64_t)(h * d * sizeof(double)), 256) +
-           (size_t)(h * quads_per_pair(d) * sizeof(uint16_t)) + 256;
+           (size_t)(h * flag_stride(d) * sizeof(uint16_t)) + 256;
 }
 
 extern "C" int temo_offspring_ws_range(const temo_problem *prob, const temo_variation *var, const double *X,
@@ -1715,7 +2534,7 @@ extern "C" int temo_offspring_ws_range(const temo_problem *prob, const temo_vari
     TEMO_LAUNCH_CHECK();
     stage_end(S_OFFSPRING, s);
     stage_begin(S_OFFSPRING_APPLY, s);
-    const size_t sm_a = 3 * d * sizeof(double) + d + 16;
+    const size_t sm_a = 3 * d * sizeof(double) + (OFF_APPLY_CSTORE ? RW * 256 * sizeof(double) : 0) + d + 16;
     const unsigned grid = (unsigned)(want < num_sms() * 3 * 8 ? want : num_sms() * 3 * 8);
     double *FOk = fused_eval(prob) ? FO : nullptr;
 #define APPLY_CASE(MM)                                                                              \

@@ -34,6 +34,19 @@ def main(path):
             if k in hdr:
                 i = hdr.index(k)
                 print(f"  {k:80s} {r[i]:>16s} {units[i]}")
+        # every other unit throughput above 25 % of its peak (which memory/pipe unit is the limiter)
+        hot = []
+        for i, k in enumerate(hdr):
+            if k in KEYS or "pct_of_peak_sustained" not in k or "throughput" not in k:
+                continue
+            try:
+                v = float(r[i])
+            except ValueError:
+                continue
+            if v >= 25.0:
+                hot.append((v, k))
+        for v, k in sorted(hot, reverse=True)[:20]:
+            print(f"  [hot] {k:74s} {v:16.2f} %")
 
 
 if __name__ == "__main__":

@@ -211,9 +211,11 @@ def test_sbx_beta_fast_vs_numpy(cuda):
                                             ("dtlz2", 3, 12, 1000, 3), ("dtlz7", 3, 13, 3, 0),
                                             ("lsmop6", 3, 1000, 40, 1), ("lsmop8", 5, 700, 33, 0)])
 def test_offspring_two_phase_equals_fused(cuda, name, m, d, h, pre):
-    """temo_offspring_ws (randomness kernel + streaming apply kernel, the harness path) is
-    bit-identical to the fused temo_offspring for every stream alignment (``pre`` shifts the
-    host Generator's buffered words) and falls back to the fused kernel when h*d % 4 != 0."""
+    """temo_offspring_ws (randomness kernel + streaming apply kernel, the harness path) gives
+    bit-identical children to the fused temo_offspring for every stream alignment (``pre``
+    shifts the host Generator's buffered words) and falls back to the fused kernel when
+    h*d % 4 != 0; objectives are bit-identical too below d = 128 (same lane layout) and agree
+    to 1e-13 above it (the gene-major apply kernel sums the groups in another order)."""
     import torch
 
     from paper_2503_20286_b200 import _lib
@@ -249,7 +251,11 @@ def test_offspring_two_phase_equals_fused(cuda, name, m, d, h, pre):
     (O1, F1) = outs[0]
     assert not np.isnan(O1).any() and not np.isnan(F1).any()
     for O2, F2 in outs[1:]:
-        assert np.array_equal(O1, O2) and np.array_equal(F1, F2)
+        assert np.array_equal(O1, O2)
+        if path_d := (d >= 128 and (h * d) % 4 == 0):  # gene-major apply kernel: sums in another order
+            assert np.allclose(F1, F2, rtol=1e-13, atol=0), path_d
+        else:
+            assert np.array_equal(F1, F2)
 
 
 @pytest.mark.parametrize("alg", ["nsga3", "hype"])
