@@ -23,6 +23,8 @@ import dataclasses
 import json
 import math
 import platform
+import queue
+import threading
 import time
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -275,6 +277,56 @@ class _Stepper:
         perm = rng_permutation(gen, n + 2 * h) if shuffle and self.config.algorithm == "nsga3" else None
         return HostInputs(p[: 2 * h].astype(np.int64), state, off, perm)
 
+    def start_host_pipeline(self, gen, steps: int, depth: int = 3) -> None:
+        """NSGA-III: draw the host inputs of the next ``steps`` generations on a worker thread
+        (in the reference's order; the permutations run in native code without the GIL), so
+        the host's sequential shuffles overlap the GPU's generations.  ``step`` consumes them
+        in order; the Generator must not be used elsewhere until they are consumed (after
+        ``steps`` generations it is in exactly the state the sequential loop leaves)."""
+        if self.config.algorithm != "nsga3" or steps <= 0:
+            return
+        self.stop_host_pipeline()
+        q: queue.Queue = queue.Queue(maxsize=depth)
+        stop = threading.Event()
+
+        def work():
+            for _ in range(steps):
+                if stop.is_set():
+                    return
+                q.put(self.draw_host_inputs(gen))
+
+        th = threading.Thread(target=work, daemon=True)
+        th.start()
+        self._pipe = [q, th, stop, steps]
+
+    def stop_host_pipeline(self) -> None:
+        pipe = getattr(self, "_pipe", None)
+        if pipe is None:
+            return
+        q, th, stop, _ = pipe
+        stop.set()
+        while th.is_alive():  # unblock a worker waiting on a full queue
+            try:
+                q.get(timeout=0.01)
+            except queue.Empty:
+                pass
+        self._pipe = None
+
+    def _next_piped(self):
+        """The next pipelined host inputs, uploaded through the pinned ring (None if no pipeline)."""
+        pipe = getattr(self, "_pipe", None)
+        if pipe is None:
+            return None
+        hi = pipe[0].get()
+        pipe[3] -= 1
+        if pipe[3] == 0:
+            pipe[1].join()
+            self._pipe = None
+        h = self.n // 2
+        self.ring.upload(hi.i12, self.i12[: 2 * h])
+        self.ring.upload(hi.shuffle, self.perm)
+        return HostInputs(self.i12, hi.state, hi.off, self.perm)
+
     def upload_host_inputs(self, inputs: list) -> list:
         """Device-resident copies of pre-drawn host inputs (bench: inputs in HBM before timing)."""
         t = _lib.torch()
@@ -404,6 +456,8 @@ class _Stepper:
         else:
             if pre is not None and alg != "nsga3":
                 raise ValueError("pre-drawn host inputs are supported for NSGA-III only")
+            if pre is None and alg == "nsga3":
+                pre = self._next_piped()
             if pre is None:
                 self._offspring(st, gen)
             else:
@@ -554,6 +608,7 @@ def run(config: RunConfig, deadline: float | None = None) -> RunRecord:
     for rep in range(config.repeats):
         gen = root.split(rep).generator()
         st = stepper.init(gen)
+        stepper.start_host_pipeline(gen, config.generations)
         F = stepper.objectives(st)
         gi, gh = metrics.measure(F)
         record = RepeatRecord(rep, {"igd": gi, "hv": gh, "ideal": F.min(dim=0).values.cpu().numpy().tolist()})
@@ -570,6 +625,7 @@ def run(config: RunConfig, deadline: float | None = None) -> RunRecord:
             if deadline is not None and time.perf_counter() > deadline:
                 record.timed_out = True
                 break
+        stepper.stop_host_pipeline()
         F = stepper.objectives(st)
         record.final_igd, record.final_hv = metrics.measure(F)
         if record.rows:
