@@ -597,6 +597,15 @@ def bench_ndsort(args, c, dev, probes, barrier, max_over_ranks):
     F = Fh.to(dev)
     rank_out = (torch.empty(N, dtype=torch.int32, device=dev), torch.empty(1, dtype=torch.int32, device=dev),
                 torch.empty(1, dtype=torch.int32, device=dev))
+    if ws > 1 and m >= 4:  # column-sharded bitmap sort: each rank owns an equal triangle area
+        from paper_2503_20286_b200.parallel import DistRank
+
+        dr = DistRank(N, m, rank, ws, dev)
+
+        def rank_device(Fd, n, mode, out):  # noqa: F811
+            r, l, nf = dr(Fd, n, mode)
+            out[0].copy_(r)
+            out[2].fill_(int(nf))
     for _ in range(args.warmup):
         rank_device(F, N, SORT, out=rank_out)
     launches = count_launches(lambda: rank_device(F, N, SORT, out=rank_out))
@@ -635,7 +644,9 @@ def bench_ndsort(args, c, dev, probes, barrier, max_over_ranks):
         "metric": c["metric"], "value": pairs / (ms * 1e-3), "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_config(args), fronts=fronts),
+        "config": dict(workload_config(args), fronts=fronts,
+                       sharding=("column tiles (bitmap, per-front mask all-gather)" if ws > 1 and m >= 4
+                                 else "replicated" if ws > 1 else "single GPU")),
         "e2e": {"value": pairs / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": N * m * 8, "d2h_bytes_per_step": N * 4},
         "roofline": hbm, "roofline_compute": comp,
         "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},

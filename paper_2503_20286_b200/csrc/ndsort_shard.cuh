@@ -250,7 +250,8 @@ __global__ void k_shard_finish(const int32_t *__restrict__ rank_s, const int32_t
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= N) return;
     const int32_t r = rank_s[p];
-    rank[order[p]] = r < 0 ? *fill : r;
+    // unranked rows, and (SELECT with batched fronts) rows ranked after the stop front, get fill
+    rank[order[p]] = (r < 0 || r > *fill) ? *fill : r;
 }
 
 static bool shard_ok(int64_t N, int m, int64_t jt_lo, int64_t jt_hi) {

@@ -107,6 +107,7 @@ class CudaShardBackend:
         self.total = t.zeros(1, dtype=t.int32, device=self.dev)
         self.fill = t.zeros(1, dtype=t.int32, device=self.dev)
         self.rank = t.empty(N, dtype=t.int32, device=self.dev)
+        self.totals = t.zeros(N + 64, dtype=t.int32, device=self.dev)  # row count of front k at [k] (+ batch slack)
         self.status = t.zeros(1, dtype=t.int32, device=self.dev)
         L = _lib.lib()
         # empty shards still need K0 + rank bookkeeping: give them a one-block dummy range
@@ -134,11 +135,13 @@ class CudaShardBackend:
         return self.seg, self.count
 
     def apply(self, full, k: int):
-        rc = _lib.lib().temo_rank_shard_apply(*self._a(), _lib.ptr(full), int(k), _lib.ptr(self.total),
+        """Rank front k everywhere and subtract its rows; returns its row count (device, [k])."""
+        out = self.totals[k: k + 1]
+        rc = _lib.lib().temo_rank_shard_apply(*self._a(), _lib.ptr(full), int(k), _lib.ptr(out),
                                               _lib.ptr(self.ws), self.ws.numel(),
                                               _lib.stream_handle(self.dev))
         _lib.check(rc, "rank_shard_apply")
-        return self.total
+        return out
 
     def finish(self, fill: int):
         self.fill.fill_(int(fill))
@@ -182,47 +185,61 @@ def assemble(bounds, segs, W, like):
     return full
 
 
-def run_sharded(backend, exchange, N: int, n: int, mode: int = SORT):
+def _front_loop(round_fn, N: int, n: int, mode: int, batch: int):
+    """Host side of the sharded peel: enqueue rounds (detect -> mask exchange -> apply) for
+    fronts k, k+1, ... in batches of 1, 2, 4 .. ``batch`` and read their row counts back once per
+    batch (one host sync per batch instead of per front).  Rounds past the end are no-ops (no
+    unranked row has a zero count); in SELECT mode rows ranked past the stop front are reset to
+    l + 1 by the finish kernel (SORT passes the front count, which no rank reaches).  Returns (l, number of fronts)."""
+    t = _lib.torch()
+    k, ranked, l, B = 0, 0, -1, 1
+    while True:
+        outs = [round_fn(k + b) for b in range(B)]
+        vals = t.cat([o.reshape(-1)[:1] for o in outs]).cpu().tolist()
+        for b, total in enumerate(vals):
+            kk = k + b
+            if total == 0:
+                if ranked < N:
+                    raise RuntimeError("front peeling failed to terminate")
+                return l, kk
+            ranked += int(total)
+            if l < 0 and ranked >= n:
+                l = kk
+            if (mode == SELECT and ranked >= n) or ranked >= N:
+                return l, kk + 1
+        k += B
+        B = min(2 * B, max(int(batch), 1))
+
+
+def run_sharded(backend, exchange, N: int, n: int, mode: int = SORT, batch: int = 8):
     """Front loop of one rank; returns (rank in original order, l, number of fronts)."""
-    k, ranked, l = 0, 0, -1
-    while True:
+
+    def round_fn(k):
         seg, _ = backend.detect(k)
-        full = exchange(seg)
-        total = int(backend.apply(full, k).item())
-        if total == 0:
-            if ranked < N:
-                raise RuntimeError("front peeling failed to terminate")
-            break
-        ranked += total
-        if l < 0 and ranked >= n:
-            l = k
-        k += 1
-        if (mode == SELECT and ranked >= n) or ranked >= N:
-            break
-    return backend.finish(l + 1), l, k
+        return backend.apply(exchange(seg), k)
+
+    l, nf = _front_loop(round_fn, N, n, mode, batch)
+    return backend.finish(l + 1 if mode == SELECT else nf), l, nf
 
 
-def run_lockstep(backends, bounds, N: int, n: int, mode: int = SORT):
+def run_lockstep(backends, bounds, N: int, n: int, mode: int = SORT, batch: int = 8):
     """G shards in one process, advanced together (single-GPU test of the shard kernels)."""
-    k, ranked, l = 0, 0, -1
     W = mask_words(N)
-    while True:
+    t = _lib.torch()
+
+    def round_fn(k):
         segs = [b.detect(k)[0] for b in backends]
         full = assemble(bounds, segs, W, segs[0] if segs[0].numel() else backends[0].seg)
-        totals = [int(b.apply(full, k).item()) for b in backends]
-        assert len(set(totals)) == 1
-        total = totals[0]
-        if total == 0:
-            if ranked < N:
-                raise RuntimeError("front peeling failed to terminate")
-            break
-        ranked += total
-        if l < 0 and ranked >= n:
-            l = k
-        k += 1
-        if (mode == SELECT and ranked >= n) or ranked >= N:
-            break
-    return [b.finish(l + 1) for b in backends], l, k
+        totals = t.cat([b.apply(full, k).reshape(-1)[:1] for b in backends])
+        return totals
+
+    def checked(k):
+        tot = round_fn(k)
+        assert bool((tot == tot[0]).all())
+        return tot[:1]
+
+    l, nf = _front_loop(checked, N, n, mode, batch)
+    return [b.finish(l + 1 if mode == SELECT else nf) for b in backends], l, nf
 
 
 class DistRank:

@@ -28,8 +28,11 @@ def test_lockstep_shards_equal_single_gpu(cuda, N, m, G, mode):
     backends = [CudaShardBackend(N, m, lo, hi) for lo, hi in bounds]
     for b in backends:
         b.build(Fd)
-    ranks, l, nf = run_lockstep(backends, bounds, N, n, mode)
-    assert l == int(l_want.item()) and nf == int(nf_want.item())
     w = want.cpu().numpy()
-    for r in ranks:
-        assert np.array_equal(r.cpu().numpy(), w)
+    for batch in (1, 8):  # host read per front / per batch of fronts
+        for b in backends:
+            b.build(Fd)
+        ranks, l, nf = run_lockstep(backends, bounds, N, n, mode, batch=batch)
+        assert l == int(l_want.item()) and nf == int(nf_want.item())
+        for r in ranks:
+            assert np.array_equal(r.cpu().numpy(), w)

@@ -54,7 +54,7 @@ class NumpyShardBackend:
         return torch.tensor([front.size])
 
     def finish(self, fill):
-        r = np.where(self.rank < 0, fill, self.rank)
+        r = np.where((self.rank < 0) | (self.rank > fill), fill, self.rank)
         out = np.empty(self.N, dtype=np.int64)
         out[self.order] = r
         return torch.from_numpy(out)
@@ -84,8 +84,10 @@ def _worker(rank, world, port, cases, q):
         be = NumpyShardBackend(N, m, lo, hi)
         be.build(F)
         ex = TorchDistExchange(bounds, mask_words(N), torch.device("cpu"))
-        r, l, nf = run_sharded(be, ex, N, n, SELECT if mode else SORT)
-        out.append((r.numpy(), l, nf))
+        for batch in (1, 8):  # one host read per front, and per batch of fronts
+            be.build(F)
+            r, l, nf = run_sharded(be, ex, N, n, SELECT if mode else SORT, batch=batch)
+            out.append((r.numpy(), l, nf))
     q.put((rank, out))
     dist.destroy_process_group()
 
@@ -101,7 +103,7 @@ def test_sharded_rank_two_processes():
     res = dict(q.get(timeout=600) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    for ci, (N, m, n, seed, mode) in enumerate(cases):
+    for ci, (N, m, n, seed, mode) in enumerate([c for c in cases for _ in (1, 8)]):
         F = np.random.default_rng(seed).random((N, m))
         if seed % 2:
             F = np.round(F, 1)
