@@ -515,7 +515,7 @@ def bench_run(args, c, dev, probes, barrier, max_over_ranks):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for g in range(args.steps):
-        st, _ = stepper.step(st, g, gen, timed=False, pre=pre[g])
+        st, _ = stepper.step(st, g, gen, timed=False, pre=pre[g], pre_next=pre[g + 1] if g + 1 < args.steps else None)
     e1.record()
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))

@@ -266,6 +266,18 @@ int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const
 /* Row-sharded form: only the pairs [q0, q1) of the h pairs, with exactly the
  * draws and output rows the full call gives them (Philox elements are indexed by the global
  * pair), so G ranks covering [0, h) together produce the full result bit for bit. */
+/* The two phases of temo_offspring_ws_range as separate calls (same workspace), so the
+ * randomness of the next generation can run on a side stream while this generation's
+ * selection runs (it needs no parent data).  Only when temo_offspring_two_phase(h, d). */
+int temo_offspring_two_phase(int64_t h, int64_t d);
+int temo_offspring_rand_ws(const temo_variation *var, int64_t d, int64_t h, int64_t q0, int64_t q1,
+                           const temo_philox_state *st, uint64_t off, void *ws, size_t ws_bytes,
+                           temo_stream_t stream);
+int temo_offspring_apply_ws(const temo_problem *prob, const temo_variation *var, const double *X,
+                            const int64_t *i1, const int64_t *i2, int64_t h, int64_t q0, int64_t q1,
+                            const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                            const int64_t *src_map, const int64_t *dst_rows, void *ws, size_t ws_bytes,
+                            temo_stream_t stream);
 int temo_offspring_ws_range(const temo_problem *prob, const temo_variation *var, const double *X,
                             const int64_t *i1, const int64_t *i2, int64_t h, int64_t q0, int64_t q1,
                             const temo_philox_state *st, uint64_t off, double *O, double *FO,

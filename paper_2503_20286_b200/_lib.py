@@ -77,6 +77,9 @@ SIGNATURES = {
     "temo_offspring": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _U64, _P, _P, _P]),
     "temo_offspring_ws_bytes": (_SZ, [_I64, _I64]),
     "temo_offspring_ws": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _U64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "temo_offspring_two_phase": (_I32, [_I64, _I64]),
+    "temo_offspring_rand_ws": (_I32, [_P, _I64, _I64, _I64, _I64, _P, _U64, _P, _SZ, _P]),
+    "temo_offspring_apply_ws": (_I32, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _U64, _P, _P, _P, _P, _P, _SZ, _P]),
     "temo_offspring_ws_range": (_I32, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _U64, _P, _P, _P, _P, _P, _SZ,
                                        _P]),
     "temo_pool_update_ws_bytes": (_SZ, [_I64]),

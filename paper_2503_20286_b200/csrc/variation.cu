@@ -2153,6 +2153,12 @@ static bool offspring_s_disabled() {
     return v == 1;
 }
 
+// integer knob from the environment, read once per process (A/B experiments; default otherwise)
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+}
+
 // TEMO_APPLY_VEC=0 disables the vector gene-major apply kernel (d even, >= 128) (A/B)
 static bool apply_vec() {
     static int v = -1;
@@ -2293,7 +2299,8 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
             TEMO_CUDA(cudaFuncSetAttribute(k_offspring_apply_v<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_v));
         }
         const int64_t want = (q1 - q0 + RW - 1) / RW;
-        const unsigned gv = (unsigned)(want < num_sms() * OFF_APPLYV_MINB * 8 ? want : num_sms() * OFF_APPLYV_MINB * 8);
+        const int64_t capv = (int64_t)num_sms() * (env_int("TEMO_APPLY_GRID_PER_SM", OFF_APPLYV_MINB * 8));
+        const unsigned gv = (unsigned)(want < capv ? want : capv);
         if (prob->id == TEMO_PROB_LSMOP1)
             k_offspring_apply_v<M, true><<<gv, RW * 32, sm_v, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
                                                                 gene_swap, beta, flags, O, FO, src_map, dst_rows);
@@ -2502,7 +2509,45 @@ extern "C" size_t temo_offspring_ws_bytes(int64_t h, int64_t d) {
            (size_t)(h * flag_stride(d) * sizeof(uint16_t)) + 256;
 }
 
-extern "C" int temo_offspring_ws_range(const temo_problem *prob, const temo_variation *var, const double *X,
+// two-phase path: congruent streams (one Philox block per quad) and staged constants
+extern "C" int temo_offspring_two_phase(int64_t h, int64_t d) {
+    return h >= 0 && d >= 1 && (h * d) % 4 == 0 && d <= SMAX_D;
+}
+
+static void offspring_ws_split(void *ws, int64_t h, int64_t d, double **beta, uint16_t **flags) {
+    *beta = static_cast<double *>(ws);
+    *flags = reinterpret_cast<uint16_t *>(static_cast<char *>(ws) + round_up((int64_t)(h * d * sizeof(double)), 256));
+}
+
+// phase 1 of temo_offspring_ws_range: randomness of pairs [q0, q1) into the workspace
+extern "C" int temo_offspring_rand_ws(const temo_variation *var, int64_t d, int64_t h, int64_t q0, int64_t q1,
+                                      const temo_philox_state *st, uint64_t off, void *ws, size_t ws_bytes,
+                                      temo_stream_t stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!var || !st || h < 0 || d < 1 || q0 < 0 || q1 > h || q0 > q1) return TEMO_EINVAL;
+    if (!temo_offspring_two_phase(h, d)) return TEMO_EINVAL;
+    if (q1 == q0) return TEMO_OK;
+    if (!ws || ws_bytes < temo_offspring_ws_bytes(h, d)) return TEMO_EWORKSPACE;
+    double *beta;
+    uint16_t *flags;
+    offspring_ws_split(ws, h, d, &beta, &flags);
+    const Philox ph = philox_from(*st);
+    const VarArgs V = var_args(var);
+    const int64_t want = (q1 - q0 + RW - 1) / RW;
+    stage_begin(S_OFFSPRING, s);
+    const int64_t capr = (int64_t)num_sms() * env_int("TEMO_RAND_GRID_PER_SM", 4 * 8);
+    const unsigned grid = (unsigned)(want < capr ? want : capr);
+    if (var->gene_swap)
+        k_offspring_rand<true><<<grid, RW * 32, 0, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
+    else
+        k_offspring_rand<false><<<grid, RW * 32, 0, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
+    TEMO_LAUNCH_CHECK();
+    stage_end(S_OFFSPRING, s);
+    return TEMO_OK;
+}
+
+// phase 2: children (and objectives) of pairs [q0, q1) from the parents and the workspace
+extern "C" int temo_offspring_apply_ws(const temo_problem *prob, const temo_variation *var, const double *X,
                                        const int64_t *i1, const int64_t *i2, int64_t h, int64_t q0, int64_t q1,
                                        const temo_philox_state *st, uint64_t off, double *O, double *FO,
                                        const int64_t *src_map, const int64_t *dst_rows,
@@ -2510,29 +2555,16 @@ extern "C" int temo_offspring_ws_range(const temo_problem *prob, const temo_vari
     cudaStream_t s = (cudaStream_t)stream;
     if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !st || !O) return TEMO_EINVAL;
     if (q0 < 0 || q1 > h || q0 > q1) return TEMO_EINVAL;
-    if (q1 == q0) return TEMO_OK;
     const int64_t d = prob->d;
-    // two-phase path needs congruent streams (one Philox block per quad) and staged constants
-    if ((h * d) % 4 != 0 || d > SMAX_D) {
-        if (src_map || dst_rows || q0 != 0 || q1 != h) return TEMO_EINVAL;  // row maps / ranges: two-phase only
-        return launch_offspring(prob, var, X, i1, i2, h, st, off, O, FO, 0, s);
-    }
+    if (!temo_offspring_two_phase(h, d)) return TEMO_EINVAL;
+    if (q1 == q0) return TEMO_OK;
     if (!ws || ws_bytes < temo_offspring_ws_bytes(h, d)) return TEMO_EWORKSPACE;
-    double *beta = static_cast<double *>(ws);
-    uint16_t *flags = reinterpret_cast<uint16_t *>(static_cast<char *>(ws) + round_up((int64_t)(h * d * sizeof(double)), 256));
+    double *beta;
+    uint16_t *flags;
+    offspring_ws_split(ws, h, d, &beta, &flags);
     const Philox ph = philox_from(*st);
     const VarArgs V = var_args(var);
     const int64_t want = (q1 - q0 + RW - 1) / RW;
-    stage_begin(S_OFFSPRING, s);
-    {
-        const unsigned grid = (unsigned)(want < num_sms() * 4 * 8 ? want : num_sms() * 4 * 8);
-        if (var->gene_swap)
-            k_offspring_rand<true><<<grid, RW * 32, 0, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
-        else
-            k_offspring_rand<false><<<grid, RW * 32, 0, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
-    }
-    TEMO_LAUNCH_CHECK();
-    stage_end(S_OFFSPRING, s);
     stage_begin(S_OFFSPRING_APPLY, s);
     const size_t sm_a = 3 * d * sizeof(double) + (OFF_APPLY_CSTORE ? RW * 256 * sizeof(double) : 0) + d + 16;
     const unsigned grid = (unsigned)(want < num_sms() * 3 * 8 ? want : num_sms() * 3 * 8);
@@ -2552,6 +2584,26 @@ extern "C" int temo_offspring_ws_range(const temo_problem *prob, const temo_vari
     }
     stage_end(S_OFFSPRING_APPLY, s);
     return TEMO_OK;
+}
+
+extern "C" int temo_offspring_ws_range(const temo_problem *prob, const temo_variation *var, const double *X,
+                                       const int64_t *i1, const int64_t *i2, int64_t h, int64_t q0, int64_t q1,
+                                       const temo_philox_state *st, uint64_t off, double *O, double *FO,
+                                       const int64_t *src_map, const int64_t *dst_rows,
+                                       void *ws, size_t ws_bytes, temo_stream_t stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !st || !O) return TEMO_EINVAL;
+    if (q0 < 0 || q1 > h || q0 > q1) return TEMO_EINVAL;
+    if (q1 == q0) return TEMO_OK;
+    const int64_t d = prob->d;
+    if (!temo_offspring_two_phase(h, d)) {
+        if (src_map || dst_rows || q0 != 0 || q1 != h) return TEMO_EINVAL;  // row maps / ranges: two-phase only
+        return launch_offspring(prob, var, X, i1, i2, h, st, off, O, FO, 0, s);
+    }
+    const int rc = temo_offspring_rand_ws(var, d, h, q0, q1, st, off, ws, ws_bytes, stream);
+    if (rc) return rc;
+    return temo_offspring_apply_ws(prob, var, X, i1, i2, h, q0, q1, st, off, O, FO, src_map, dst_rows, ws,
+                                   ws_bytes, stream);
 }
 
 extern "C" int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const double *X,

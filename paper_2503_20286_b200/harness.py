@@ -198,6 +198,16 @@ class _Stepper:
         self.off_ws = t.empty(max(int(_lib.lib().temo_offspring_ws_bytes(self.h, d)), 256),
                               dtype=t.uint8, device=self.dev)
         self.perm = t.empty(self.N, dtype=t.int64, device=self.dev)
+        # TEMO_OVERLAP_RAND=1|2: run the next generation's offspring randomness on a side stream
+        # (needs its host inputs drawn ahead: pre-drawn lists or the host pipeline), overlapping
+        # this generation's apply + selection (1) or apply only (2).  Off by default: measured
+        # 7.4-11 ms vs 5.3 ms per generation at pop 200k -- the compute-bound randomness CTAs
+        # take the SMs from the latency-bound K0 sorts and the cooperative peel
+        # (scripts/ab_overlap.sh, profiles/r02_overlap_ab.txt).
+        import os
+
+        self.overlap = int(os.environ.get("TEMO_OVERLAP_RAND", "0"))
+        self._gen_k, self._rand_ahead, self._apply_done, self._side = 0, None, None, None
         alg = config.algorithm
         # multi-GPU: one process per GPU, every rank runs the same host RNG stream;
         # offspring rows and HypE sample columns are sharded, the bitmap ND sort (m >= 4) too
@@ -277,6 +287,11 @@ class _Stepper:
         perm = rng_permutation(gen, n + 2 * h) if shuffle and self.config.algorithm == "nsga3" else None
         return HostInputs(p[: 2 * h].astype(np.int64), state, off, perm)
 
+    def _side_stream(self):
+        if self._side is None:
+            self._side = _lib.torch().cuda.Stream(device=self.dev)
+        return self._side
+
     def start_host_pipeline(self, gen, steps: int, depth: int = 3) -> None:
         """NSGA-III: draw the host inputs of the next ``steps`` generations on a worker thread
         (in the reference's order; the permutations run in native code without the GIL), so
@@ -300,6 +315,7 @@ class _Stepper:
         self._pipe = [q, th, stop, steps]
 
     def stop_host_pipeline(self) -> None:
+        self._look = None
         pipe = getattr(self, "_pipe", None)
         if pipe is None:
             return
@@ -312,20 +328,27 @@ class _Stepper:
                 pass
         self._pipe = None
 
-    def _next_piped(self):
-        """The next pipelined host inputs, uploaded through the pinned ring (None if no pipeline)."""
-        pipe = getattr(self, "_pipe", None)
-        if pipe is None:
-            return None
+    def _pipe_get(self):
+        pipe = self._pipe
         hi = pipe[0].get()
         pipe[3] -= 1
         if pipe[3] == 0:
             pipe[1].join()
             self._pipe = None
+        return hi
+
+    def _next_piped(self):
+        """(this generation's pipelined host inputs uploaded through the pinned ring, the next
+        generation's host inputs or None); (None, None) without a pipeline."""
+        look = getattr(self, "_look", None)
+        if getattr(self, "_pipe", None) is None and look is None:
+            return None, None
+        hi = look if look is not None else self._pipe_get()
+        self._look = self._pipe_get() if getattr(self, "_pipe", None) is not None else None
         h = self.n // 2
         self.ring.upload(hi.i12, self.i12[: 2 * h])
         self.ring.upload(hi.shuffle, self.perm)
-        return HostInputs(self.i12, hi.state, hi.off, self.perm)
+        return HostInputs(self.i12, hi.state, hi.off, self.perm), self._look
 
     def upload_host_inputs(self, inputs: list) -> list:
         """Device-resident copies of pre-drawn host inputs (bench: inputs in HBM before timing)."""
@@ -337,7 +360,23 @@ class _Stepper:
             out.append(HostInputs(i12, hi.state, hi.off, sh))
         return out
 
-    def _offspring(self, st: DeviceState, gen, pre: HostInputs | None = None):
+    def _rand_ws(self, k: int):
+        """Offspring randomness workspace of generation k (two, alternating, when the next
+        generation's randomness runs ahead on the side stream)."""
+        t = _lib.torch()
+        if k % 2 == 0:
+            return self.off_ws
+        if getattr(self, "off_ws_b", None) is None:
+            self.off_ws_b = t.empty_like(self.off_ws)
+        return self.off_ws_b
+
+    def _launch_rand(self, hi: HostInputs, h: int, q0: int, q1: int, k: int, stream) -> None:
+        ws = self._rand_ws(k)
+        rc = _lib.lib().temo_offspring_rand_ws(_lib.sptr(self.var), self.spec.d, h, q0, q1, _lib.sptr(hi.state),
+                                               hi.off, _lib.ptr(ws), ws.numel(), stream)
+        _lib.check(rc, "offspring_rand")
+
+    def _offspring(self, st: DeviceState, gen, pre: HostInputs | None = None, pre_next: HostInputs | None = None):
         n = st.n  # RVEA's population is the number of non-empty partitions (<= self.n)
         if n < 2:
             return self._mutate_in_place(st, gen)
@@ -362,13 +401,48 @@ class _Stepper:
             from .parallel import shard_range
 
             q0, q1 = shard_range(h, *self.shard)
-        rc = _lib.lib().temo_offspring_ws_range(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
-                                                _lib.ptr(i12), _lib.ptr(i12[h:]), h, q0, q1,
-                                                _lib.sptr(pre.state), off, obase,
-                                                _lib.ptr(cur.F[n:]), src, dst,
-                                                _lib.ptr(self.off_ws), self.off_ws.numel(),
-                                                _lib.stream_handle(self.dev))
-        _lib.check(rc, "offspring")
+        t = _lib.torch()
+        L = _lib.lib()
+        if pooled and n == self.n and L.temo_offspring_two_phase(h, self.spec.d):
+            # randomness of generation k (launched ahead on the side stream, or now), then this
+            # generation's apply; the next generation's randomness (inputs drawn ahead) goes to
+            # the side stream at once -- it needs no parent data, so it overlaps the apply and
+            # the selection (SM time the latency-bound selection leaves idle)
+            k = self._gen_k
+            main = t.cuda.current_stream(self.dev)
+            ahead = self._rand_ahead
+            if ahead is not None and ahead[0] == k and ahead[2].state is pre.state and ahead[2].off == pre.off:
+                main.wait_event(ahead[1])
+            else:
+                self._launch_rand(pre, h, q0, q1, k, _lib.stream_handle(self.dev))
+            self._rand_ahead = None
+            if pre_next is not None and self.overlap:
+                side = self._side_stream()
+                if self._apply_done is not None:  # the workspace of k + 1 was last read by apply k - 1
+                    side.wait_event(self._apply_done)
+                self._launch_rand(pre_next, h, q0, q1, k + 1, side.cuda_stream)
+                ev = t.cuda.Event()
+                ev.record(side)
+                self._rand_ahead = (k + 1, ev, pre_next)
+            ws = self._rand_ws(k)
+            rc = L.temo_offspring_apply_ws(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
+                                           _lib.ptr(i12), _lib.ptr(i12[h:]), h, q0, q1, _lib.sptr(pre.state), off,
+                                           obase, _lib.ptr(cur.F[n:]), src, dst, _lib.ptr(ws), ws.numel(),
+                                           _lib.stream_handle(self.dev))
+            _lib.check(rc, "offspring")
+            if self.overlap == 2 and self._rand_ahead is not None:  # overlap the apply only
+                main.wait_event(self._rand_ahead[1])
+            self._apply_done = t.cuda.Event()
+            self._apply_done.record(main)
+            self._gen_k = k + 1
+        else:
+            rc = L.temo_offspring_ws_range(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
+                                           _lib.ptr(i12), _lib.ptr(i12[h:]), h, q0, q1,
+                                           _lib.sptr(pre.state), off, obase,
+                                           _lib.ptr(cur.F[n:]), src, dst,
+                                           _lib.ptr(self.off_ws), self.off_ws.numel(),
+                                           _lib.stream_handle(self.dev))
+            _lib.check(rc, "offspring")
         st.extra["N_cur"] = n + 2 * h
         if (q0, q1) != (0, h):
             self._exchange_children(st, n, h)
@@ -434,7 +508,8 @@ class _Stepper:
         """X of the current offspring (logical rows [n, N))."""
         return st.rows(st.n, st.extra.get("N_cur", self.N))
 
-    def step(self, st: DeviceState, g: int, gen, timed: bool = True, pre: HostInputs | None = None):
+    def step(self, st: DeviceState, g: int, gen, timed: bool = True, pre: HostInputs | None = None,
+             pre_next: HostInputs | None = None):
         """One generation (harness.py:206-248); returns (state, seconds).
 
         ``seconds`` is the device time of the whole step -- or of the selection alone with
@@ -442,7 +517,8 @@ class _Stepper:
         the step).  ``timed=False`` returns at once with ``seconds = None`` (launch-ahead loops).
         ``pre``: this generation's host inputs drawn ahead by ``draw_host_inputs`` and made
         device-resident by ``upload_host_inputs`` (NSGA-III; the Generator must already be past
-        them)."""
+        them); ``pre_next``: the next generation's (its offspring randomness is then launched on
+        the side stream during this step)."""
         t = _lib.torch()
         alg = self.config.algorithm
         ev = [t.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
@@ -457,11 +533,11 @@ class _Stepper:
             if pre is not None and alg != "nsga3":
                 raise ValueError("pre-drawn host inputs are supported for NSGA-III only")
             if pre is None and alg == "nsga3":
-                pre = self._next_piped()
+                pre, pre_next = self._next_piped()
             if pre is None:
                 self._offspring(st, gen)
             else:
-                self._offspring(st, gen, pre)
+                self._offspring(st, gen, pre, pre_next)
             if timed:
                 ev[1].record()
             cur, nxt = st.cur, st.nxt
