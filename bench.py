@@ -539,7 +539,6 @@ def bench_run(args, c, dev, probes, barrier, max_over_ranks):
     d2h = F_host[0].numel() * 8
     barrier()
     t0 = time.perf_counter()
-    stepper.start_host_pipeline(gen, args.steps)  # NSGA-III: host shuffles on a worker thread
     for g in range(args.steps):
         st, _ = stepper.step(st, g, gen, timed=False)  # host draws of step g+1 overlap step g on the GPU
         F_host[g % (LAG + 1)].copy_(stepper.objectives(st), non_blocking=True)

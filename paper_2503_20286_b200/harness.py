@@ -295,7 +295,9 @@ class _Stepper:
     def start_host_pipeline(self, gen, steps: int, depth: int = 3) -> None:
         """NSGA-III: draw the host inputs of the next ``steps`` generations on a worker thread
         (in the reference's order; the permutations run in native code without the GIL), so
-        the host's sequential shuffles overlap the GPU's generations.  ``step`` consumes them
+        the host's sequential shuffles overlap the GPU's generations.  Opt-in: at pop 200k the
+        worker's NumPy work contends with the launching thread for the GIL and the e2e loop
+        measured 143-153 gen/s with it vs 163 without.  ``step`` consumes them
         in order; the Generator must not be used elsewhere until they are consumed (after
         ``steps`` generations it is in exactly the state the sequential loop leaves)."""
         if self.config.algorithm != "nsga3" or steps <= 0:
@@ -684,7 +686,6 @@ def run(config: RunConfig, deadline: float | None = None) -> RunRecord:
     for rep in range(config.repeats):
         gen = root.split(rep).generator()
         st = stepper.init(gen)
-        stepper.start_host_pipeline(gen, config.generations)
         F = stepper.objectives(st)
         gi, gh = metrics.measure(F)
         record = RepeatRecord(rep, {"igd": gi, "hv": gh, "ideal": F.min(dim=0).values.cpu().numpy().tolist()})

@@ -299,3 +299,31 @@ def test_row_pool_equals_survivor_copy(cuda, alg):
         runs.append(traj)
     for (Xa, Fa), (Xb, Fb) in zip(*runs):
         assert np.array_equal(Xa, Xb) and np.array_equal(Fa, Fb)
+
+
+@pytest.mark.parametrize("overlap", [0, 1])
+def test_host_pipeline_and_overlap_equivalence(cuda, overlap):
+    """The opt-in host-input pipeline (worker thread) and the side-stream randomness overlap
+    give the sequential loop's populations and leave the Generator in the same state."""
+    import json
+
+    from paper_2503_20286_b200.harness import RunConfig, _resolve, _Stepper
+    from paper_2503_20286_b200.rng import RngStream
+
+    cfg = RunConfig(algorithm="nsga3", problem="lsmop1", objectives=3, dim=300, pop_size=400, seed=2)
+    spec, R, n = _resolve(cfg)
+    outs = []
+    for mode in ("plain", "pipe"):
+        st_ = _Stepper(cfg, spec, R, n)
+        st_.overlap = overlap if mode == "pipe" else 0
+        gen = RngStream(2).split(0).generator()
+        st = st_.init(gen)
+        if mode == "pipe":
+            st_.start_host_pipeline(gen, 4)
+        for g in range(4):
+            st, _ = st_.step(st, g, gen, timed=False)
+        X, F = st_.population(st)
+        state = json.dumps(gen.bit_generator.state, default=lambda a: np.asarray(a).tolist())
+        outs.append((X.cpu().numpy(), F.cpu().numpy(), state))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
