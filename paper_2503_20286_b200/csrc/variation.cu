@@ -20,6 +20,12 @@
 
 namespace temo {
 
+// integer knob from the environment (A/B experiments; the default otherwise)
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+}
+
 constexpr int VT = 128;
 constexpr double PI = 3.141592653589793;
 
@@ -2153,12 +2159,6 @@ static bool offspring_s_disabled() {
     return v == 1;
 }
 
-// integer knob from the environment, read once per process (A/B experiments; default otherwise)
-static int env_int(const char *name, int dflt) {
-    const char *e = getenv(name);
-    return (e && *e) ? atoi(e) : dflt;
-}
-
 // TEMO_APPLY_VEC=0 disables the vector gene-major apply kernel (d even, >= 128) (A/B)
 static bool apply_vec() {
     static int v = -1;
@@ -2240,7 +2240,8 @@ int eval_m(const temo_problem *prob, const double *X, const int64_t *map, int64_
            int64_t c2, double *F, cudaStream_t s) {
     const int64_t n = c1 + c2;
     if (n <= 0) return TEMO_OK;
-    if (prob->id > TEMO_PROB_LSMOP1) {  // LSMOP2..9: warp per row
+    if (prob->id > TEMO_PROB_LSMOP1 || (prob->id == TEMO_PROB_LSMOP1 && env_int("TEMO_LSMOP1_WARP_EVAL", 0))) {
+        // LSMOP: warp per row
         const int64_t want = (n + 7) / 8;
         const unsigned grid = (unsigned)(want < num_sms() * 8 * 4 ? want : num_sms() * 8 * 4);
         k_eval_lsmop<M><<<grid, 256, 0, s>>>(*prob, X, map, lo1, c1, lo2, c2, F);
@@ -2470,8 +2471,11 @@ extern "C" int temo_pm(const temo_variation *var, const double *X, int64_t rows,
     return TEMO_OK;
 }
 
-// LSMOP2..9 are evaluated by a separate warp-per-row pass over the children (no fused sums)
-static bool fused_eval(const temo_problem *prob) { return prob->id <= TEMO_PROB_LSMOP1; }
+// LSMOP2..9 are evaluated by a separate warp-per-row pass over the children (no fused sums);
+// TEMO_SPLIT_EVAL=1 does the same for LSMOP1 (A/B of the apply kernel without its sums)
+static bool fused_eval(const temo_problem *prob) {
+    return prob->id < TEMO_PROB_LSMOP1 || (prob->id == TEMO_PROB_LSMOP1 && !env_int("TEMO_SPLIT_EVAL", 0));
+}
 
 static int launch_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
                             const int64_t *i1, const int64_t *i2, int64_t h,
