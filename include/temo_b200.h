@@ -308,6 +308,14 @@ int temo_pool_update(const int64_t *phys, const int64_t *perm, const int32_t *ke
  * kind: TEMO_AGG_PBI (reference) or TEMO_AGG_TCH (new; parity unpinned). */
 #define TEMO_AGG_PBI 0
 #define TEMO_AGG_TCH 1
+/* temo_moead_offspring with the Philox state read from device memory (st_dev: a
+ * temo_philox_state in device memory), so the generation can be captured once in a CUDA
+ * graph and replayed with each generation's state.  TEMO_EINVAL unless the staged kernel
+ * applies (n*d % 4 == 0, d <= 3000). */
+int temo_moead_offspring_dev(const temo_problem *prob, const temo_variation *var, const double *X,
+                             const int64_t *p1, const int64_t *p2, int64_t n,
+                             const temo_philox_state *st_dev, uint64_t off, double *O, double *FO,
+                             temo_stream_t stream);
 int temo_moead_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
                          const int64_t *p1, const int64_t *p2, int64_t n,
                          const temo_philox_state *st, uint64_t off, double *O, double *FO,

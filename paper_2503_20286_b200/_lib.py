@@ -85,6 +85,7 @@ SIGNATURES = {
     "temo_pool_update_ws_bytes": (_SZ, [_I64]),
     "temo_pool_update": (_I32, [_P, _P, _P, _I64, _I64, _P, _P, _P, _SZ, _P]),
     "temo_init_population": (_I32, [_P, _U64, _I64, _I64, _P, _P, _P, _P]),
+    "temo_moead_offspring_dev": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _U64, _P, _P, _P]),
     "temo_moead_offspring": (_I32, [_P, _P, _P, _P, _P, _I64, _P, _U64, _P, _P, _P]),
     "temo_moead_compare": (_I32, [_P, _P, _P, _P, _I64, _I32, _I32, _P, _D, _I32, _P, _P, _P, _P]),
     "temo_moead_elite": (_I32, [_P, _P, _P, _P, _P, _I64, _I64, _I32, _I32, _P, _D, _I32, _P, _P, _P,

@@ -862,15 +862,22 @@ static __device__ __noinline__ double sbx_beta(double mu, double e) {
 }
 constexpr int SMAX_D = 3000;     // genes staged in shared memory (else k_offspring_w)
 
-template <int M, bool SWAP>
+// DEVST: the Philox state is read from device memory (st_dev) instead of the launch
+// parameters, so a captured CUDA graph can replay the kernel with each generation's state
+template <int M, bool SWAP, bool DEVST = false>
 __global__ void __launch_bounds__(SW * 32, OFF_S_MINB) k_offspring_s(temo_problem P, VarArgs V,
                                                             const double *__restrict__ X,
                                                             const int64_t *__restrict__ i1,
                                                             const int64_t *__restrict__ i2, int64_t h,
-                                                            Philox ph, uint64_t off,
+                                                            const __grid_constant__ Philox ph_arg,
+                                                            const temo_philox_state *__restrict__ st_dev,
+                                                            uint64_t off,
                                                             double *__restrict__ O,
                                                             double *__restrict__ FO, int single) {
     extern __shared__ double ssm[];
+    __shared__ Philox s_ph;
+    if (DEVST && threadIdx.x == 0) s_ph = philox_from(*st_dev);  // published by the barrier below
+    const Philox &ph = DEVST ? s_ph : ph_arg;
     const int64_t d = P.d;
     double *s_lo = ssm, *s_hi = ssm + d, *s_cf = ssm + 2 * d;
     double *s_q = ssm + 3 * d + (threadIdx.x >> 5) * 128;  // per-warp pow queue
@@ -2255,23 +2262,35 @@ template <int M>
 int offspring_m(const temo_problem *prob, const temo_variation *var, const double *X,
                 const int64_t *i1, const int64_t *i2, int64_t h, const temo_philox_state *st,
                 uint64_t off, double *O, double *FO, int single, bool warp_path, size_t smem,
-                int smem_rows, cudaStream_t s) {
+                int smem_rows, cudaStream_t s, const temo_philox_state *st_dev) {
     const int64_t d = prob->d;
     if (warp_path && d <= SMAX_D && !offspring_s_disabled()) {
         const size_t sm_s = (3 * d + SW * 128) * sizeof(double) + d + 16;
         if (sm_s > 48 * 1024) {
             TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
             TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<M, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+            TEMO_CUDA(cudaFuncSetAttribute(k_offspring_s<M, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
         }
         const int64_t want = (h + SW - 1) / SW;
         const unsigned grid = (unsigned)(want < num_sms() * 2 * 4 ? want : num_sms() * 2 * 4);
-        if (var->gene_swap)
-            k_offspring_s<M, true><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h,
-                                                               philox_from(*st), off, O, FO, single);
+        const Philox ph = st_dev ? Philox{} : philox_from(*st);
+        if (st_dev && var->gene_swap)
+            k_offspring_s<M, true, true><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h, ph, st_dev,
+                                                                     off, O, FO, single);
+        else if (st_dev)
+            k_offspring_s<M, false, true><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h, ph, st_dev,
+                                                                      off, O, FO, single);
+        else if (var->gene_swap)
+            k_offspring_s<M, true><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h, ph, nullptr,
+                                                               off, O, FO, single);
         else
-            k_offspring_s<M, false><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h,
-                                                                philox_from(*st), off, O, FO, single);
-    } else if (warp_path && var->gene_swap) {
+            k_offspring_s<M, false><<<grid, SW * 32, sm_s, s>>>(*prob, var_args(var), X, i1, i2, h, ph, nullptr,
+                                                                off, O, FO, single);
+        return TEMO_OK;
+    }
+    if (st_dev) return TEMO_EINVAL;  // device-resident state: the staged kernel only
+    if (warp_path && var->gene_swap) {
         k_offspring_w<M, true><<<(unsigned)((h + OW - 1) / OW), OW * 32, 0, s>>>(
             *prob, var_args(var), X, i1, i2, h, philox_from(*st), off, O, FO, single);
     } else if (warp_path) {
@@ -2360,7 +2379,7 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
     EXT template int offspring_m<MM>(const temo_problem *, const temo_variation *, const double *,   \
                                      const int64_t *, const int64_t *, int64_t,                      \
                                      const temo_philox_state *, uint64_t, double *, double *, int,    \
-                                     bool, size_t, int, cudaStream_t);                                \
+                                     bool, size_t, int, cudaStream_t, const temo_philox_state *);     \
     EXT template int apply_m<MM>(const temo_problem *, const VarArgs &, const double *,              \
                                  const int64_t *, const int64_t *, int64_t, int64_t, int64_t,         \
                                  const Philox &, uint64_t,                                             \
@@ -2480,8 +2499,8 @@ static bool fused_eval(const temo_problem *prob) {
 static int launch_offspring(const temo_problem *prob, const temo_variation *var, const double *X,
                             const int64_t *i1, const int64_t *i2, int64_t h,
                             const temo_philox_state *st, uint64_t off, double *O, double *FO,
-                            int single, cudaStream_t s) {
-    if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !st || !O) return TEMO_EINVAL;
+                            int single, cudaStream_t s, const temo_philox_state *st_dev = nullptr) {
+    if (!prob_ok(prob) || !var || !X || !i1 || !i2 || h < 0 || !(st || st_dev) || !O) return TEMO_EINVAL;
     if (h == 0) return TEMO_OK;
     const int64_t d = prob->d;
     const int smem_rows = 2 * d * (int64_t)sizeof(double) <= 96 * 1024;
@@ -2493,7 +2512,7 @@ static int launch_offspring(const temo_problem *prob, const temo_variation *var,
 #define OFF_CASE(MM)                                                                               \
     case MM: {                                                                                     \
         int rc = offspring_m<MM>(prob, var, X, i1, i2, h, st, off, O, FOk, single, warp_path, smem, \
-                                 smem_rows, s);                                                    \
+                                 smem_rows, s, st_dev);                                            \
         if (rc) return rc;                                                                         \
     } break;
     TEMO_M_SWITCH(prob->m, OFF_CASE)
@@ -2624,6 +2643,15 @@ extern "C" int temo_offspring(const temo_problem *prob, const temo_variation *va
                               const temo_philox_state *st, uint64_t off, double *O, double *FO,
                               temo_stream_t stream) {
     return launch_offspring(prob, var, X, i1, i2, h, st, off, O, FO, 0, (cudaStream_t)stream);
+}
+
+// temo_moead_offspring with the Philox state in device memory (CUDA-graph capturable)
+extern "C" int temo_moead_offspring_dev(const temo_problem *prob, const temo_variation *var,
+                                        const double *X, const int64_t *p1, const int64_t *p2, int64_t n,
+                                        const temo_philox_state *st_dev, uint64_t off, double *O, double *FO,
+                                        temo_stream_t stream) {
+    if (!st_dev) return TEMO_EINVAL;
+    return launch_offspring(prob, var, X, p1, p2, n, nullptr, off, O, FO, 1, (cudaStream_t)stream, st_dev);
 }
 
 extern "C" int temo_moead_offspring(const temo_problem *prob, const temo_variation *var,

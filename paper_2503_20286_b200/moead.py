@@ -16,6 +16,7 @@ import numpy as np
 
 from . import _lib
 from .rng import DeviceDraws, is_philox
+from .rng import PhiloxState as _PhiloxState
 
 KINDS = {"pbi": 0, "tch": 1}
 
@@ -127,6 +128,11 @@ class MoeadEngine:
         self.ring = _lib.HostRing()
         self.var = params.struct(d, self.dev)
         self.prob = spec.struct()
+        # one CUDA graph per state parity (TEMO_MOEAD_GRAPH=0: plain launches)
+        import os
+
+        self.graph = os.environ.get("TEMO_MOEAD_GRAPH", "1") != "0"
+        self._gbuf, self._graphs = None, [None, None]
 
     def init_state(self, X, F1):
         t = _t()
@@ -144,6 +150,10 @@ class MoeadEngine:
         self.ring.upload(par, self.parents)
         draws = DeviceDraws(gen)
         off = draws.take(5 * n * self.spec.d if self.params.gene_swap else 3 * n * self.spec.d)
+        if self.graph and off == 0 and (n * self.spec.d) % 4 == 0 and self.spec.d <= 3000:
+            out = self._step_graph(st, draws)
+            draws.commit()
+            return out
         L = _lib.lib()
         p = _lib.ptr
         rc = L.temo_moead_offspring(_lib.sptr(self.prob), _lib.sptr(self.var), p(st.X), p(self.parents),
@@ -152,6 +162,67 @@ class MoeadEngine:
         _lib.check(rc, "moead_offspring")
         draws.commit()
         return self.select(st, self.O, self.F2)
+
+    # -- CUDA-graph generation (moead.py:148-158 as one graph replay per step)
+    def _graph_buffers(self, st: MoeadState):
+        t = _t()
+        if self._gbuf is None:
+            self._gbuf = ([t.empty_like(st.X) for _ in range(2)], [t.empty_like(st.F1) for _ in range(2)],
+                          [t.empty_like(self.zmin) for _ in range(2)],
+                          t.zeros(ctypes.sizeof(_PhiloxState), dtype=t.uint8, device=self.dev))
+        gX, gF, gz, _ = self._gbuf
+        for p in (0, 1):  # the state already lives in a graph buffer: replay that parity's graph
+            if st.X.data_ptr() == gX[p].data_ptr() and st.F1.data_ptr() == gF[p].data_ptr() \
+                    and st.z.data_ptr() == gz[p].data_ptr():
+                return p
+        gX[0].copy_(st.X)
+        gF[0].copy_(st.F1)
+        gz[0].copy_(st.z)
+        return 0
+
+    def _capture(self, p: int):
+        t = _t()
+        gX, gF, gz, st_dev = self._gbuf
+        q = 1 - p
+        L, ptr = _lib.lib(), _lib.ptr
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g, capture_error_mode="thread_local"):
+            h = _lib.stream_handle(self.dev)
+            rc = L.temo_moead_offspring_dev(_lib.sptr(self.prob), _lib.sptr(self.var), ptr(gX[p]), ptr(self.parents),
+                                            ptr(self.parents[self.n:]), self.n, ptr(st_dev), 0, ptr(self.O),
+                                            ptr(self.F2), h)
+            _lib.check(rc, "moead_offspring")
+            self._select_into(gX[p], gF[p], gz[p], self.O, self.F2, gX[q], gF[q], h)
+            gz[q].copy_(self.zmin)
+        return g
+
+    def _step_graph(self, st: MoeadState, draws):
+        """One generation as a CUDA-graph replay: the pairing indices and the Philox state are
+        uploaded to fixed device buffers (stream-ordered), then one graph runs offspring +
+        compare + elite.  The state ping-pongs between two buffer sets, one graph per parity;
+        a returned state stays valid until two more steps have run."""
+        p = self._graph_buffers(st)
+        gX, gF, gz, st_dev = self._gbuf
+        raw = np.frombuffer(ctypes.string_at(ctypes.addressof(draws.state), ctypes.sizeof(draws.state)),
+                            dtype=np.uint8)
+        self.ring.upload(raw, st_dev)
+        if self._graphs[p] is None:
+            self._graphs[p] = self._capture(p)
+        self._graphs[p].replay()
+        q = 1 - p
+        return MoeadState(gX[q], gF[q], gz[q], st.W, st.I_nb, st.theta)
+
+    def _select_into(self, X, F1, z, O, F2, Xn, Fn, h):
+        L, p = _lib.lib(), _lib.ptr
+        n, T = self.n, self.T
+        m, d = F2.shape[1], O.shape[1]
+        rc = L.temo_moead_compare(p(F1), p(F2), p(self.W), p(self.I_nb), n, T, m, p(z), self.theta, self.kind,
+                                  p(self.zmin), p(self.g_new), p(self.improves), h)
+        _lib.check(rc, "compare_update")
+        rc = L.temo_moead_elite(p(X), p(F1), p(self.W), p(O), p(F2), n, d, T, m, p(self.zmin), self.theta,
+                                self.kind, p(self.rptr), p(self.rcol), p(self.g_new), p(self.improves),
+                                p(self.winner), p(Xn), p(Fn), h)
+        _lib.check(rc, "elite_select")
 
     def select(self, st: MoeadState, O, F2):
         """compare_update + elite_select + z update on device tensors."""
