@@ -1648,12 +1648,9 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLY_MINB) k_offspring_apply_t(t
 #ifndef OFF_APPLYV_MINB
 #define OFF_APPLYV_MINB 3
 #endif
-static __device__ __noinline__ double pm_gene(const Philox &ph, int64_t e_quad, int64_t avail, int bit, double c,
-                                              double lo, double hi, double eta) {
-    uint64_t m[4];
-    raw_quad(ph, e_quad, avail, m);
-    return clipv(pm_step(c, lo, hi, u01(pick4u(m, bit)), eta), lo, hi);
-}
+#ifndef OFF_PMFIX_MINB
+#define OFF_PMFIX_MINB 4
+#endif
 
 template <int M, bool LSMOP>
 __global__ void __launch_bounds__(RW * 32, OFF_APPLYV_MINB) k_offspring_apply_v(temo_problem P, VarArgs V,
@@ -1722,6 +1719,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLYV_MINB) k_offspring_apply_v(
             const int b0 = g0 & 3, b1 = (g0 + 1) & 3;
             double y[2][2];
             const double av[2] = {a.x, a.y}, bv[2] = {b.x, b.y}, sv[2] = {bb.x, bb.y};
+            uint32_t hitm = 0;  // bit 2 e + c: gene 2 v + e of child c is a PM hit
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const uint32_t w = e ? w1 : w0;
@@ -1737,9 +1735,9 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLYV_MINB) k_offspring_apply_v(
                     const double lo = s_lo[g], hi = s_hi[g];
                     y1 = clipv(y1, lo, hi);
                     y2 = clipv(y2, lo, hi);
-                    const int64_t eq = q * d + g - bit;  // start of the gene's stream quad
-                    if ((w >> (4 + bit)) & 1) y1 = pm_gene(ph, o_pmu + eq, avail, bit, y1, lo, hi, eta);
-                    if ((w >> (8 + bit)) & 1) y2 = pm_gene(ph, o_pmu + hd + eq, avail, bit, y2, lo, hi, eta);
+                    // PM hits are applied by k_offspring_pm_fix (their terms are added there)
+                    hitm |= ((w >> (4 + bit)) & 1u) << (2 * e);
+                    hitm |= ((w >> (8 + bit)) & 1u) << (2 * e + 1);
                 }
                 y[0][e] = y1;
                 y[1][e] = y2;
@@ -1757,6 +1755,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLYV_MINB) k_offspring_apply_v(
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int64_t g = 2 * v + e;
+                const bool h1 = (hitm >> (2 * e)) & 1, h2 = (hitm >> (2 * e + 1)) & 1;
                 if constexpr (LSMOP) {
                     const int grp = (int)s_grp[g];
                     if (grp < 0) continue;
@@ -1766,12 +1765,12 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLYV_MINB) k_offspring_apply_v(
 #pragma unroll
                     for (int i = 0; i < M; ++i)
                         if (grp == i) {
-                            part1[i] += xa * xa;
-                            part2[i] += xb * xb;
+                            if (!h1) part1[i] += xa * xa;
+                            if (!h2) part2[i] += xb * xb;
                         }
                 } else {
-                    acc_gene<M>(P, g, y[0][e], x0a, part1);
-                    acc_gene<M>(P, g, y[1][e], x0b, part2);
+                    if (!h1) acc_gene<M>(P, g, y[0][e], x0a, part1);
+                    if (!h2) acc_gene<M>(P, g, y[1][e], x0b, part2);
                 }
             }
         }
@@ -1783,17 +1782,202 @@ __global__ void __launch_bounds__(RW * 32, OFF_APPLYV_MINB) k_offspring_apply_v(
                 part1[i] += __shfl_xor_sync(~0u, part1[i], s);
                 part2[i] += __shfl_xor_sync(~0u, part2[i], s);
             }
-        __syncwarp();
-        if (lane == 0) {
-            double f[M];
-            finish_objs<M>(P, reinterpret_cast<const double *>(o1), part1, f);
+        if (lane == 0) {  // the group sums of the non-hit genes; k_offspring_pm_fix finishes them
 #pragma unroll
-            for (int i = 0; i < M; ++i) FO[q * M + i] = f[i];
+            for (int i = 0; i < M; ++i) FO[q * M + i] = part1[i];
         } else if (lane == 1) {
-            double f[M];
-            finish_objs<M>(P, reinterpret_cast<const double *>(o2), part2, f);
 #pragma unroll
-            for (int i = 0; i < M; ++i) FO[(h + q) * M + i] = f[i];
+            for (int i = 0; i < M; ++i) FO[(h + q) * M + i] = part2[i];
+        }
+    }
+}
+
+// Hit list of the PM pass: thread per (pair, stream quad); warp-aggregated append of
+// (q << 13 | child << 12 | gene).  The counter keeps counting past the capacity (overflow ->
+// the per-pair pass applies the PM itself).
+static __global__ void __launch_bounds__(256) k_pm_list(int64_t d, int64_t h, int64_t q0, int64_t q1, uint64_t off,
+                                                 int ph_pos, const uint16_t *__restrict__ flags,
+                                                 int64_t *__restrict__ list, int64_t cap) {
+    const int lane = threadIdx.x & 31;
+    const int64_t QP = quads_per_pair(d), QS = flag_stride(d);
+    const int64_t items = (q1 - q0) * QP;
+    const int64_t avail = 4 - ph_pos;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < items; base += stride) {
+        const int64_t it = base + threadIdx.x;
+        int64_t q = 0, j = 0;
+        uint32_t hit = 0;
+        if (it < items) {
+            q = q0 + it / QP;
+            j = it % QP;
+            hit = (flags[q * QS + j] >> 4) & 0xFF;
+        }
+        const int sh = (int)(((int64_t)off + q * d - avail) & 3);
+        const int n = __popc(hit);
+        int incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(~0u, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(~0u, incl, 31);
+        if (total == 0) continue;
+        unsigned long long b0 = 0;
+        if (lane == 31) b0 = atomicAdd(reinterpret_cast<unsigned long long *>(list), (unsigned long long)total);
+        b0 = __shfl_sync(~0u, b0, 31);
+        int64_t w = (int64_t)b0 + incl - n;
+        for (int k = 0; k < 8; ++k) {
+            if (!((hit >> k) & 1)) continue;
+            const int c = k >> 2;
+            const int64_t g = 4 * j - sh + (k & 3);
+            if (w < cap) list[1 + w] = (q << 13) | ((int64_t)c << 12) | g;
+            ++w;
+        }
+    }
+}
+
+// PM of every listed hit (variation.py:104-120): its aligned Philox block, pm_step on the stored
+// SBX child value, the write-back.  Each entry's result is independent of the list order.
+static __global__ void __launch_bounds__(256) k_pm_apply(VarArgs V, int64_t d, int64_t h, const __grid_constant__ Philox ph,
+                                                  uint64_t off, int swap, const int64_t *__restrict__ list, int64_t cap,
+                                                  double *__restrict__ O, const int64_t *__restrict__ dst_rows) {
+    const int64_t n = list[0];
+    if (n > cap) return;  // overflow: the per-pair pass does it
+    const int64_t hd = h * d;
+    const int64_t o_mu = (int64_t)off;
+    const int64_t o_pmu = o_mu + (swap ? 3 * hd : hd);
+    const int64_t avail = 4 - ph.pos;
+    const double eta = V.eta_m + 1.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = list[1 + i];
+        const int64_t q = e >> 13, g = e & 0xFFF;
+        const int c = (int)((e >> 12) & 1);
+        const int sh = (int)((o_mu + q * d - avail) & 3);
+        const int bit = (int)((g + sh) & 3);
+        uint64_t mm[4];
+        raw_quad(ph, o_pmu + (c ? hd : 0) + q * d + g - bit, avail, mm);
+        const int64_t r = c ? h + q : q;
+        double *y = O + (dst_rows ? dst_rows[r] : r) * d + g;
+        const double lo = V.lower[g], hi = V.upper[g];
+        *y = clipv(pm_step(*y, lo, hi, u01(pick4u(mm, bit)), eta), lo, hi);
+    }
+}
+
+// PM pass after k_offspring_apply_v (warp per pair): for every hit gene of both children the
+// PM draw (its aligned Philox block), pm_step on the stored SBX child value and the write-back,
+// then the objectives from the apply kernel's sums plus the hit genes' terms.  A child whose
+// gene 0 was hit (the LSMOP linkage uses it for every gene) has its sums recomputed from its
+// row.  Children are bit-identical to the inline-PM kernels.
+template <int M, bool LSMOP>
+__global__ void __launch_bounds__(RW * 32, OFF_PMFIX_MINB) k_offspring_pm_fix(temo_problem P, VarArgs V, int64_t h, int64_t q0,
+                                                              int64_t q1, const __grid_constant__ Philox ph,
+                                                              uint64_t off, int swap,
+                                                              const uint16_t *__restrict__ flags,
+                                                              double *__restrict__ O, double *__restrict__ FO,
+                                                              const int64_t *__restrict__ dst_rows,
+                                                              const int64_t *__restrict__ pm_list, int64_t pm_cap) {
+    const bool applied = pm_list[0] <= pm_cap;  // k_pm_apply already wrote every hit's PM value
+    if (applied && !FO) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t d = P.d;
+    const int64_t hd = h * d;
+    const int64_t o_mu = (int64_t)off;
+    const int64_t o_pmu = o_mu + (swap ? 3 * hd : hd);
+    const int64_t avail = 4 - ph.pos;
+    const double eta = V.eta_m + 1.0;
+    const int64_t QP = quads_per_pair(d), QS = flag_stride(d);
+    for (int64_t q = q0 + (int64_t)blockIdx.x * RW + (threadIdx.x >> 5); q < q1; q += (int64_t)gridDim.x * RW) {
+        const uint16_t *fq = flags + q * QS;
+        const int sh = (int)((o_mu + q * d - avail) & 3);
+        double *orow[2] = {O + (dst_rows ? dst_rows[q] : q) * d, O + (dst_rows ? dst_rows[h + q] : h + q) * d};
+        // gene 0 first (its final value enters every LSMOP term)
+        const uint32_t f0 = fq[0];
+        bool dirty[2];
+        double x0[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            dirty[c] = (f0 >> (4 + 4 * c + sh)) & 1;
+            if (dirty[c] && lane == 0 && !applied) {
+                uint64_t mm[4];
+                raw_quad(ph, o_pmu + (c ? hd : 0) + q * d - sh, avail, mm);
+                const double lo = V.lower[0], hi = V.upper[0];
+                orow[c][0] = clipv(pm_step(orow[c][0], lo, hi, u01(pick4u(mm, sh)), eta), lo, hi);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) x0[c] = orow[c][0];
+        double t[2][M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) t[0][i] = t[1][i] = 0.0;
+        for (int64_t j = lane; j < QP; j += 32) {
+            const uint32_t fl = fq[j];
+            const uint32_t hit = (fl >> 4) & 0xFF;
+            if (!hit) continue;
+            const int64_t gs = 4 * j - sh;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                if (!((hit >> (4 * c)) & 0xF)) continue;
+                uint64_t mm[4];
+                if (!applied) raw_quad(ph, o_pmu + (c ? hd : 0) + q * d + gs, avail, mm);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t g = gs + k;
+                    if (!((hit >> (4 * c + k)) & 1) || g <= 0 || g >= d) continue;  // gene 0 done above
+                    double y = orow[c][g];
+                    if (!applied) {
+                        const double lo = V.lower[g], hi = V.upper[g];
+                        y = clipv(pm_step(y, lo, hi, u01(mm[k]), eta), lo, hi);
+                        orow[c][g] = y;
+                    }
+                    if (!FO || dirty[c]) continue;
+                    if constexpr (LSMOP) {
+                        const int64_t rel = g - (M - 1);
+                        const double xs = (1.0 + (double)(g + 1) / (double)d) * y - 10.0 * x0[c];
+#pragma unroll
+                        for (int i = 0; i < M; ++i)
+                            if (rel >= P.offset[i] && rel < P.offset[i + 1]) t[c][i] += xs * xs;
+                    } else {
+                        acc_gene<M>(P, g, y, x0[c], t[c]);
+                    }
+                }
+            }
+        }
+        if (!FO) continue;
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            if (dirty[c]) {  // recompute this child's sums from its final row
+#pragma unroll
+                for (int i = 0; i < M; ++i) t[c][i] = 0.0;
+                for (int64_t g = lane; g < d; g += 32) {
+                    const double y = orow[c][g];
+                    if constexpr (LSMOP) {
+                        const int64_t rel = g - (M - 1);
+                        if (rel < 0) continue;
+                        const double xs = (1.0 + (double)(g + 1) / (double)d) * y - 10.0 * x0[c];
+#pragma unroll
+                        for (int i = 0; i < M; ++i)
+                            if (rel >= P.offset[i] && rel < P.offset[i + 1]) t[c][i] += xs * xs;
+                    } else {
+                        acc_gene<M>(P, g, y, x0[c], t[c]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+#pragma unroll
+                for (int s = 16; s; s >>= 1) t[c][i] += __shfl_xor_sync(~0u, t[c][i], s);
+        }
+        if (lane < 2) {
+            const int c = lane;
+            double part[M], f[M];
+            double *fo = FO + ((c ? h : 0) + q) * M;
+#pragma unroll
+            for (int i = 0; i < M; ++i) part[i] = (dirty[c] ? 0.0 : fo[i]) + t[c][i];
+            finish_objs<M>(P, orow[c], part, f);
+#pragma unroll
+            for (int i = 0; i < M; ++i) fo[i] = f[i];
         }
     }
 }
@@ -2310,7 +2494,7 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
             const int64_t *i2, int64_t h, int64_t q0, int64_t q1, const Philox &ph, uint64_t off, int gene_swap,
             const double *beta, const uint16_t *flags, double *O, double *FO,
             const int64_t *src_map, const int64_t *dst_rows, size_t sm_a, unsigned grid,
-            cudaStream_t s) {
+            cudaStream_t s, int64_t *pm_list, int64_t pm_cap) {
     const int64_t d = prob->d;
     if (d >= 128 && d % 2 == 0 && apply_vec()) {
         const size_t sm_v = 3 * d * sizeof(double) + d + 16;
@@ -2321,12 +2505,28 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
         const int64_t want = (q1 - q0 + RW - 1) / RW;
         const int64_t capv = (int64_t)num_sms() * (env_int("TEMO_APPLY_GRID_PER_SM", OFF_APPLYV_MINB * 8));
         const unsigned gv = (unsigned)(want < capv ? want : capv);
+        const int64_t wantf = (q1 - q0 + RW - 1) / RW;
+        const unsigned gf = (unsigned)wantf;
+        // PM hits: compacted list (order irrelevant: each entry's result is fixed), one thread per
+        // hit, then per pair the objectives from the apply sums + the hit genes' terms in gene order
+        TEMO_CUDA(cudaMemsetAsync(pm_list, 0, sizeof(int64_t), s));
+        const int64_t items = (q1 - q0) * quads_per_pair(d);
+        const unsigned gl = (unsigned)((items + 255) / 256 < num_sms() * 32 ? (items + 255) / 256 : num_sms() * 32);
+        const unsigned gp = (unsigned)((pm_cap + 255) / 256 < num_sms() * 16 ? (pm_cap + 255) / 256 : num_sms() * 16);
         if (prob->id == TEMO_PROB_LSMOP1)
             k_offspring_apply_v<M, true><<<gv, RW * 32, sm_v, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
                                                                 gene_swap, beta, flags, O, FO, src_map, dst_rows);
         else
             k_offspring_apply_v<M, false><<<gv, RW * 32, sm_v, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
                                                                  gene_swap, beta, flags, O, FO, src_map, dst_rows);
+        k_pm_list<<<gl, 256, 0, s>>>(d, h, q0, q1, off, ph.pos, flags, pm_list, pm_cap);
+        k_pm_apply<<<gp, 256, 0, s>>>(V, d, h, ph, off, gene_swap, pm_list, pm_cap, O, dst_rows);
+        if (prob->id == TEMO_PROB_LSMOP1)
+            k_offspring_pm_fix<M, true><<<gf, RW * 32, 0, s>>>(*prob, V, h, q0, q1, ph, off, gene_swap, flags, O, FO,
+                                                               dst_rows, pm_list, pm_cap);
+        else
+            k_offspring_pm_fix<M, false><<<gf, RW * 32, 0, s>>>(*prob, V, h, q0, q1, ph, off, gene_swap, flags, O,
+                                                                FO, dst_rows, pm_list, pm_cap);
         return TEMO_OK;
     }
     if (d >= 128 && apply_gene_major()) {
@@ -2384,7 +2584,8 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
                                  const int64_t *, const int64_t *, int64_t, int64_t, int64_t,         \
                                  const Philox &, uint64_t,                                             \
                                  int, const double *, const uint16_t *, double *, double *,           \
-                                 const int64_t *, const int64_t *, size_t, unsigned, cudaStream_t);
+                                 const int64_t *, const int64_t *, size_t, unsigned, cudaStream_t, int64_t *,  \
+                                 int64_t);
 #ifdef TEMO_M_ONLY
 TEMO_VAR_DECL(TEMO_M_ONLY, )
 #else
@@ -2526,10 +2727,19 @@ static int launch_offspring(const temo_problem *prob, const temo_variation *var,
     return TEMO_OK;
 }
 
+// PM hit list of the vector apply path: a counter and up to pm_list_cap entries (expected
+// hits per generation 2 h d p_m = 2 h at the default p_m = 1/d; beyond the cap the per-pair
+// fallback applies the PM)
+static int64_t pm_list_cap(int64_t h, int64_t d) {
+    const int64_t c = 16 * h + 65536;
+    return c < 2 * h * d ? c : 2 * h * d;
+}
+
 extern "C" size_t temo_offspring_ws_bytes(int64_t h, int64_t d) {
     if (h < 0 || d < 1) return 0;
     return (size_t)round_up((int64_t)(h * d * sizeof(double)), 256) +
-           (size_t)(h * flag_stride(d) * sizeof(uint16_t)) + 256;
+           (size_t)round_up((int64_t)(h * flag_stride(d) * sizeof(uint16_t)), 256) +
+           (size_t)((1 + pm_list_cap(h, d)) * sizeof(int64_t)) + 256;
 }
 
 // two-phase path: congruent streams (one Philox block per quad) and staged constants
@@ -2537,9 +2747,14 @@ extern "C" int temo_offspring_two_phase(int64_t h, int64_t d) {
     return h >= 0 && d >= 1 && (h * d) % 4 == 0 && d <= SMAX_D;
 }
 
-static void offspring_ws_split(void *ws, int64_t h, int64_t d, double **beta, uint16_t **flags) {
-    *beta = static_cast<double *>(ws);
-    *flags = reinterpret_cast<uint16_t *>(static_cast<char *>(ws) + round_up((int64_t)(h * d * sizeof(double)), 256));
+static void offspring_ws_split(void *ws, int64_t h, int64_t d, double **beta, uint16_t **flags,
+                               int64_t **pm_list = nullptr) {
+    char *b = static_cast<char *>(ws);
+    *beta = reinterpret_cast<double *>(b);
+    b += round_up((int64_t)(h * d * sizeof(double)), 256);
+    *flags = reinterpret_cast<uint16_t *>(b);
+    b += round_up((int64_t)(h * flag_stride(d) * sizeof(uint16_t)), 256);
+    if (pm_list) *pm_list = reinterpret_cast<int64_t *>(b);
 }
 
 // phase 1 of temo_offspring_ws_range: randomness of pairs [q0, q1) into the workspace
@@ -2584,10 +2799,12 @@ extern "C" int temo_offspring_apply_ws(const temo_problem *prob, const temo_vari
     if (!ws || ws_bytes < temo_offspring_ws_bytes(h, d)) return TEMO_EWORKSPACE;
     double *beta;
     uint16_t *flags;
-    offspring_ws_split(ws, h, d, &beta, &flags);
+    int64_t *pm_list;
+    offspring_ws_split(ws, h, d, &beta, &flags, &pm_list);
     const Philox ph = philox_from(*st);
     const VarArgs V = var_args(var);
     const int64_t want = (q1 - q0 + RW - 1) / RW;
+    const int64_t pm_cap = pm_list_cap(h, d);
     stage_begin(S_OFFSPRING_APPLY, s);
     const size_t sm_a = 3 * d * sizeof(double) + (OFF_APPLY_CSTORE ? RW * 256 * sizeof(double) : 0) + d + 16;
     const unsigned grid = (unsigned)(want < num_sms() * 3 * 8 ? want : num_sms() * 3 * 8);
@@ -2595,7 +2812,7 @@ extern "C" int temo_offspring_apply_ws(const temo_problem *prob, const temo_vari
 #define APPLY_CASE(MM)                                                                              \
     case MM: {                                                                                      \
         int rc = apply_m<MM>(prob, V, X, i1, i2, h, q0, q1, ph, off, var->gene_swap, beta, flags, O, FOk, \
-                             src_map, dst_rows, sm_a, grid, s);                                     \
+                             src_map, dst_rows, sm_a, grid, s, pm_list, pm_cap);                    \
         if (rc) return rc;                                                                          \
     } break;
     TEMO_M_SWITCH(prob->m, APPLY_CASE)
