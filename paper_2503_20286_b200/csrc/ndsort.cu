@@ -18,6 +18,7 @@
 //       round trips (ndsort.py:60-69).
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -36,6 +37,7 @@ constexpr int LC = 8 * ROWS_PER_WARP;    // K2 (shard path): list rows per work 
 constexpr int PEEL_RPW = 30 * PEEL_HALVES;  // K2: rows per warp per item, resolved 30 at a time (<= 255)
 constexpr int PEEL_LC = 8 * PEEL_RPW;       // K2: rows per item (cross-warp sums unpacked to int)
 constexpr int MAX_M = 16;
+constexpr int K0_LANES = 3;  // K0: column rank sorts in flight at once (latency-bound at N <= 500k)
 
 #ifndef TEMO_M_ONLY
 int num_sms() {
@@ -68,8 +70,30 @@ struct RankPlan {
     uint32_t *bits;    // packed triangular bitmap
     int32_t *cnt, *rank_s, *list, *blkcnt;
     void *cub_tmp;
+    // K0 column lanes 1..K0_LANES-1 (lane 0 is keys_a .. cub_tmp above): own sort scratch,
+    // so the per-column rank sorts run concurrently on side streams
+    uint64_t *lk_a[K0_LANES], *lk_b[K0_LANES];
+    int32_t *lv_a[K0_LANES], *lv_b[K0_LANES], *ls_a[K0_LANES], *ls_b[K0_LANES];
+    void *ltmp[K0_LANES];
     size_t total;
 };
+
+// K0 lane scratch (after keys_a .. cub_tmp are carved): lane 0 aliases the main buffers
+static void take_k0_lanes(RankPlan &p, Carve &c) {
+    p.lk_a[0] = p.keys_a; p.lk_b[0] = p.keys_b; p.lv_a[0] = p.vals_a; p.lv_b[0] = p.vals_b;
+    p.ls_a[0] = p.scan_a; p.ls_b[0] = p.scan_b; p.ltmp[0] = p.cub_tmp;
+    for (int l = 1; l < K0_LANES; ++l) {
+        const bool use = l < p.m;
+        const int64_t n = use ? p.N : 0;
+        p.lk_a[l] = c.take<uint64_t>(n);
+        p.lk_b[l] = c.take<uint64_t>(n);
+        p.lv_a[l] = c.take<int32_t>(n);
+        p.lv_b[l] = c.take<int32_t>(n);
+        p.ls_a[l] = c.take<int32_t>(n);
+        p.ls_b[l] = c.take<int32_t>(n);
+        p.ltmp[l] = c.take<char>(use ? p.cub_bytes : 0);
+    }
+}
 
 static int64_t bitmap_words(int64_t nT, int64_t W) {
     // row tile I stores words [8I, W) for its 256 rows
@@ -125,7 +149,44 @@ static void plan_rank(RankPlan &p, void *base, int64_t N, int m) {
     p.list = c.take<int32_t>(p.Np);
     p.blkcnt = c.take<int32_t>(p.NB + 1);
     p.cub_tmp = c.take<char>(p.cub_bytes);
+    take_k0_lanes(p, c);
     p.total = c.off;
+}
+
+// Side streams + fork/join events of the concurrent K0 column sorts: created once per host
+// thread and device (stream/event handles, no device memory); the fork/join pattern is
+// legal inside CUDA-graph stream capture.  TEMO_K0_LANES=1 keeps everything on one stream.
+struct K0Side {
+    cudaStream_t s[K0_LANES];
+    cudaEvent_t fork, join[K0_LANES];
+    bool ready = false;
+};
+
+static int k0_lanes_env() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_K0_LANES");
+        v = e ? atoi(e) : K0_LANES;
+        if (v < 1) v = 1;
+        if (v > K0_LANES) v = K0_LANES;
+    }
+    return v;
+}
+
+static K0Side *k0_side() {
+    thread_local K0Side side[16];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    K0Side &k = side[dev & 15];
+    if (!k.ready) {
+        for (int l = 1; l < K0_LANES; ++l) {
+            if (cudaStreamCreateWithFlags(&k.s[l], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+            if (cudaEventCreateWithFlags(&k.join[l], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        }
+        if (cudaEventCreateWithFlags(&k.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        k.ready = true;
+    }
+    return &k;
 }
 
 #ifndef TEMO_M_ONLY  // non-template kernels: base translation unit only
@@ -1337,14 +1398,27 @@ static int build_records(RankPlan &p, const double *F, int32_t *status, cudaStre
         else if (m == 3) k_small_k0<3><<<gb, 256, 0, st>>>(kc, N, MP, p.R, p.vals_a);
         else k_small_k0<4><<<gb, 256, 0, st>>>(kc, N, MP, p.R, p.vals_a);
     } else {
-    // K0: per-column dense ranks
+    // K0: per-column dense ranks, up to K0_LANES columns in flight (fork/join on side streams)
+    int lanes = m < k0_lanes_env() ? m : k0_lanes_env();
+    K0Side *side = lanes > 1 ? k0_side() : nullptr;
+    if (!side) lanes = 1;
+    if (lanes > 1) {
+        TEMO_CUDA(cudaEventRecord(side->fork, st));
+        for (int l = 1; l < lanes; ++l) TEMO_CUDA(cudaStreamWaitEvent(side->s[l], side->fork, 0));
+    }
     for (int col = 0; col < m; ++col) {
-        k_col_keys<<<grid1(N), 256, 0, st>>>(F, N, m, col, p.keys_a, p.vals_a, status);
-        TEMO_CUDA(cub::DeviceRadixSort::SortPairs(p.cub_tmp, tb, p.keys_a, p.keys_b, p.vals_a,
-                                                  p.vals_b, (int)N, 0, 64, st));
-        k_key_change<<<grid1(N), 256, 0, st>>>(p.keys_b, N, p.scan_a);
-        TEMO_CUDA(cub::DeviceScan::InclusiveSum(p.cub_tmp, tb, p.scan_a, p.scan_b, (int)N, st));
-        k_scatter_rank<<<grid1(N), 256, 0, st>>>(p.vals_b, p.scan_b, N, MP, col, p.R);
+        const int l = col % lanes;
+        cudaStream_t cs = l ? side->s[l] : st;
+        k_col_keys<<<grid1(N), 256, 0, cs>>>(F, N, m, col, p.lk_a[l], p.lv_a[l], status);
+        TEMO_CUDA(cub::DeviceRadixSort::SortPairs(p.ltmp[l], tb, p.lk_a[l], p.lk_b[l], p.lv_a[l],
+                                                  p.lv_b[l], (int)N, 0, 64, cs));
+        k_key_change<<<grid1(N), 256, 0, cs>>>(p.lk_b[l], N, p.ls_a[l]);
+        TEMO_CUDA(cub::DeviceScan::InclusiveSum(p.ltmp[l], tb, p.ls_a[l], p.ls_b[l], (int)N, cs));
+        k_scatter_rank<<<grid1(N), 256, 0, cs>>>(p.lv_b[l], p.ls_b[l], N, MP, col, p.R);
+    }
+    for (int l = 1; l < lanes; ++l) {
+        TEMO_CUDA(cudaEventRecord(side->join[l], side->s[l]));
+        TEMO_CUDA(cudaStreamWaitEvent(st, side->join[l], 0));
     }
     // lexicographic order of rank tuples: LSD passes, several columns per u64 key
     k_iota<<<grid1(N), 256, 0, st>>>(p.vals_a, N);

@@ -64,6 +64,7 @@ static void plan_shard(ShardPlan &s, void *base, int64_t N, int m, int64_t jt_lo
     p.rec = c.take<uint4>((size_t)p.Np * p.NV);
     take_packed(p, c);
     p.cub_tmp = c.take<char>(p.cub_bytes);
+    take_k0_lanes(p, c);
     s.off = c.take<int64_t>(p.nT + 1);
     s.lo = c.take<int64_t>(p.nT + 1);
     s.stride = c.take<int64_t>(p.nT + 1);

@@ -81,6 +81,7 @@ static void plan_k0(RankPlan &p, Carve &c, int64_t N, int m) {
     p.R = c.take<uint32_t>((size_t)N * 4 * p.NV);
     p.rec = c.take<uint4>((size_t)p.Np * p.NV);
     p.cub_tmp = c.take<char>(p.cub_bytes);
+    take_k0_lanes(p, c);
 }
 
 static void plan_stair(StairPlan &s, void *base, int64_t N, int m) {
