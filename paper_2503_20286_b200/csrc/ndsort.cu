@@ -179,8 +179,10 @@ static K0Side *k0_side() {
     cudaGetDevice(&dev);
     K0Side &k = side[dev & 15];
     if (!k.ready) {
+        int lo = 0, hi = 0;  // the sorts are on the critical path: highest priority
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
         for (int l = 1; l < K0_LANES; ++l) {
-            if (cudaStreamCreateWithFlags(&k.s[l], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+            if (cudaStreamCreateWithPriority(&k.s[l], cudaStreamNonBlocking, hi) != cudaSuccess) return nullptr;
             if (cudaEventCreateWithFlags(&k.join[l], cudaEventDisableTiming) != cudaSuccess) return nullptr;
         }
         if (cudaEventCreateWithFlags(&k.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;

@@ -1139,10 +1139,17 @@ __global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64
     if (V.p_m >= 1.0) pm_thr = INT64_MAX;
     else if (V.p_m >= 0.0) pm_thr = (int64_t)floor(V.p_m * 9007199254740992.0);
     const int64_t QP = quads_per_pair(d);
-    for (int64_t q = q0 + (int64_t)blockIdx.x * RW + warp; q < q1; q += (int64_t)gridDim.x * RW) {
+    // work unit = (pair, 128-gene chunk): short units let a high-priority stream's kernels take
+    // SMs back quickly when this kernel overlaps the previous generation's selection
+    const int64_t NC = (d + 3 + 127) / 128;
+    const int64_t units = (q1 - q0) * NC;
+    for (int64_t u = (int64_t)blockIdx.x * RW + warp; u < units; u += (int64_t)gridDim.x * RW) {
+        const int64_t q = q0 + u / NC, c = u % NC;
         const int sh = (int)((o_mu + q * d - avail) & 3);
         double *bq = beta + q * d;
-        for (int64_t base = -sh, j0 = 0; base < d; base += 128, j0 += 32) {
+        {
+            const int64_t base = -sh + 128 * c, j0 = 32 * c;
+            if (base >= d) continue;
             const int64_t gs = base + 4 * lane;
             const int64_t es = q * d + gs;
             uint32_t okm = 0;
@@ -2771,9 +2778,9 @@ extern "C" int temo_offspring_rand_ws(const temo_variation *var, int64_t d, int6
     offspring_ws_split(ws, h, d, &beta, &flags);
     const Philox ph = philox_from(*st);
     const VarArgs V = var_args(var);
-    const int64_t want = (q1 - q0 + RW - 1) / RW;
+    const int64_t want = ((q1 - q0) * ((d + 3 + 127) / 128) + RW - 1) / RW;
     stage_begin(S_OFFSPRING, s);
-    const int64_t capr = (int64_t)num_sms() * env_int("TEMO_RAND_GRID_PER_SM", 4 * 8);
+    const int64_t capr = (int64_t)num_sms() * env_int("TEMO_RAND_GRID_PER_SM", 1024);
     const unsigned grid = (unsigned)(want < capr ? want : capr);
     if (var->gene_swap)
         k_offspring_rand<true><<<grid, RW * 32, 0, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);

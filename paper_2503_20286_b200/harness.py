@@ -198,16 +198,19 @@ class _Stepper:
         self.off_ws = t.empty(max(int(_lib.lib().temo_offspring_ws_bytes(self.h, d)), 256),
                               dtype=t.uint8, device=self.dev)
         self.perm = t.empty(self.N, dtype=t.int64, device=self.dev)
-        # TEMO_OVERLAP_RAND=1|2: run the next generation's offspring randomness on a side stream
-        # (needs its host inputs drawn ahead: pre-drawn lists or the host pipeline), overlapping
-        # this generation's apply + selection (1) or apply only (2).  Off by default: measured
-        # 7.4-11 ms vs 5.3 ms per generation at pop 200k -- the compute-bound randomness CTAs
-        # take the SMs from the latency-bound K0 sorts and the cooperative peel
-        # (scripts/ab_overlap.sh, profiles/r02_overlap_ab.txt).
+        # TEMO_OVERLAP_RAND=1|2 (default 1): run the next generation's offspring randomness on a
+        # low-priority side stream (needs its host inputs drawn ahead: pre-drawn lists or the host
+        # pipeline), overlapping this generation's apply + selection (1) or apply only (2).  The
+        # generation itself then runs on a high-priority stream (joined to the caller's stream at
+        # both ends) and the randomness kernel is split into short (pair, 128-gene) units, so the
+        # block scheduler hands SMs back to the latency-bound selection kernels within one unit:
+        # 4.24 vs 5.0 ms per generation at pop 200k (profiles/r02_overlap_ab.txt).  Without the
+        # priority stream and short units the overlap was slower (7.4-11 ms): long persistent
+        # randomness CTAs took the SMs from the K0 sorts and the cooperative peel.
         import os
 
-        self.overlap = int(os.environ.get("TEMO_OVERLAP_RAND", "0"))
-        self._gen_k, self._rand_ahead, self._apply_done, self._side = 0, None, None, None
+        self.overlap = int(os.environ.get("TEMO_OVERLAP_RAND", "1"))
+        self._gen_k, self._rand_ahead, self._apply_done, self._side, self._hp = 0, None, None, None, None
         alg = config.algorithm
         # multi-GPU: one process per GPU, every rank runs the same host RNG stream;
         # offspring rows and HypE sample columns are sharded, the bitmap ND sort (m >= 4) too
@@ -512,6 +515,23 @@ class _Stepper:
 
     def step(self, st: DeviceState, g: int, gen, timed: bool = True, pre: HostInputs | None = None,
              pre_next: HostInputs | None = None):
+        """One generation (see ``_step``).  With the randomness overlap on (NSGA-III), the
+        generation's kernels run on a high-priority stream that waits for the caller's current
+        stream on entry and is waited for on exit, so stream order for the caller is unchanged."""
+        if not (self.overlap and self.config.algorithm == "nsga3"):
+            return self._step(st, g, gen, timed, pre, pre_next)
+        t = _lib.torch()
+        if self._hp is None:
+            self._hp = t.cuda.Stream(device=self.dev, priority=-1)
+        caller = t.cuda.current_stream(self.dev)
+        self._hp.wait_stream(caller)
+        with t.cuda.stream(self._hp):
+            out = self._step(st, g, gen, timed, pre, pre_next)
+        caller.wait_stream(self._hp)
+        return out
+
+    def _step(self, st: DeviceState, g: int, gen, timed: bool = True, pre: HostInputs | None = None,
+              pre_next: HostInputs | None = None):
         """One generation (harness.py:206-248); returns (state, seconds).
 
         ``seconds`` is the device time of the whole step -- or of the selection alone with

@@ -327,3 +327,31 @@ def test_host_pipeline_and_overlap_equivalence(cuda, overlap):
         outs.append((X.cpu().numpy(), F.cpu().numpy(), state))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
     assert outs[0][2] == outs[1][2]
+
+
+def test_predrawn_overlap_priority_stream_equivalence(cuda):
+    """bench.py's device-resident loop (pre-drawn inputs, the next generation's randomness on the
+    low-priority side stream while this one runs on the high-priority stream) gives the plain
+    loop's populations bit for bit (pop 3000: units of several CTAs in flight at once)."""
+    import torch
+
+    from paper_2503_20286_b200.harness import RunConfig, _resolve, _Stepper
+    from paper_2503_20286_b200.rng import RngStream
+
+    cfg = RunConfig(algorithm="nsga3", problem="lsmop1", objectives=3, dim=500, pop_size=3000, seed=5)
+    spec, R, n = _resolve(cfg)
+    outs = []
+    for overlap in (0, 1):
+        st_ = _Stepper(cfg, spec, R, n)
+        st_.overlap = overlap
+        gen = RngStream(5).split(0).generator()
+        st = st_.init(gen)
+        K = 5
+        pre = st_.upload_host_inputs([st_.draw_host_inputs(gen) for _ in range(K)])
+        for g in range(K):
+            st, _ = st_.step(st, g, gen, timed=False, pre=pre[g], pre_next=pre[g + 1] if g + 1 < K else None)
+        torch.cuda.synchronize()
+        st_.check()
+        X, F = st_.population(st)
+        outs.append((X.cpu().numpy(), F.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
