@@ -2782,10 +2782,19 @@ extern "C" int temo_offspring_rand_ws(const temo_variation *var, int64_t d, int6
     stage_begin(S_OFFSPRING, s);
     const int64_t capr = (int64_t)num_sms() * env_int("TEMO_RAND_GRID_PER_SM", 1024);
     const unsigned grid = (unsigned)(want < capr ? want : capr);
+    // TEMO_RAND_SMEM: dynamic shared memory per CTA (unused) to cap the resident randomness
+    // CTAs per SM, leaving room for overlapped selection kernels (A/B knob)
+    static const int pad = env_int("TEMO_RAND_SMEM", 0);
+    static bool attr = false;
+    if (pad > 48 * 1024 && !attr) {
+        cudaFuncSetAttribute(k_offspring_rand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+        cudaFuncSetAttribute(k_offspring_rand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+        attr = true;
+    }
     if (var->gene_swap)
-        k_offspring_rand<true><<<grid, RW * 32, 0, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
+        k_offspring_rand<true><<<grid, RW * 32, pad, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
     else
-        k_offspring_rand<false><<<grid, RW * 32, 0, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
+        k_offspring_rand<false><<<grid, RW * 32, pad, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
     TEMO_LAUNCH_CHECK();
     stage_end(S_OFFSPRING, s);
     return TEMO_OK;

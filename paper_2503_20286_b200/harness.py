@@ -210,6 +210,8 @@ class _Stepper:
         import os
 
         self.overlap = int(os.environ.get("TEMO_OVERLAP_RAND", "1"))
+        # launch the next generation's randomness after (1) or before (0) this generation's apply
+        self._rand_after_apply = os.environ.get("TEMO_RAND_AFTER_APPLY", "0") == "1"
         self._gen_k, self._rand_ahead, self._apply_done, self._side, self._hp = 0, None, None, None, None
         alg = config.algorithm
         # multi-GPU: one process per GPU, every rank runs the same host RNG stream;
@@ -421,7 +423,8 @@ class _Stepper:
             else:
                 self._launch_rand(pre, h, q0, q1, k, _lib.stream_handle(self.dev))
             self._rand_ahead = None
-            if pre_next is not None and self.overlap:
+
+            def ahead():
                 side = self._side_stream()
                 if self._apply_done is not None:  # the workspace of k + 1 was last read by apply k - 1
                     side.wait_event(self._apply_done)
@@ -429,12 +432,18 @@ class _Stepper:
                 ev = t.cuda.Event()
                 ev.record(side)
                 self._rand_ahead = (k + 1, ev, pre_next)
+
+            late = self._rand_after_apply
+            if pre_next is not None and self.overlap and not late:
+                ahead()
             ws = self._rand_ws(k)
             rc = L.temo_offspring_apply_ws(_lib.sptr(self.prob), _lib.sptr(self.var), _lib.ptr(cur.X),
                                            _lib.ptr(i12), _lib.ptr(i12[h:]), h, q0, q1, _lib.sptr(pre.state), off,
                                            obase, _lib.ptr(cur.F[n:]), src, dst, _lib.ptr(ws), ws.numel(),
                                            _lib.stream_handle(self.dev))
             _lib.check(rc, "offspring")
+            if pre_next is not None and self.overlap and late:
+                ahead()
             if self.overlap == 2 and self._rand_ahead is not None:  # overlap the apply only
                 main.wait_event(self._rand_ahead[1])
             self._apply_done = t.cuda.Event()
