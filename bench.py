@@ -199,8 +199,16 @@ def roofline_offspring(h, d, stages, steps, probes):
     quads = h * (-(-d // 4) + 1)
     blocks = 5 * h * d / 4.0
     apply_bytes = 8.0 * (2 * h * d) + 8.0 * (h * d) + 8.0 * (2 * h * d) + 2.0 * quads  # parents, beta, children, flags
+    vec_ms = stages.get("apply_vec", (0.0, 1))[0] / steps
     hbm = None
-    if apply_ms > 0:
+    if vec_ms > 0:  # the streaming kernel of the apply stage, timed alone (its own events)
+        ach = apply_bytes / (vec_ms * 1e-3) / 1e9
+        hbm = {"bound": "hbm", "kernel": "k_offspring_apply_v (SBX apply + LSMOP sums, streaming)", "achieved": ach,
+               "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic("k_offspring_apply_v", 2 * h),
+               "algorithmic_bytes": apply_bytes, "avg_launch_ms": vec_ms, "peak_source": src,
+               "stage": {"name": "offspring_apply (apply_v + PM hit list + PM/objective pass)",
+                         "ms": apply_ms, "achieved": apply_bytes / (apply_ms * 1e-3) / 1e9 if apply_ms > 0 else None}}
+    elif apply_ms > 0:
         ach = apply_bytes / (apply_ms * 1e-3) / 1e9
         hbm = {"bound": "hbm", "kernel": "k_offspring_apply (SBX/PM apply + evaluation)", "achieved": ach,
                "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic("k_offspring_apply", 2 * h),
@@ -550,27 +558,34 @@ def bench_run(args, c, dev, probes, barrier, max_over_ranks):
     else:
         h2d = 8 * 2 * n  # MOEA/D parent rows from the two integers draws
     d2h = F_host[0].numel() * 8
+    # the e2e loop runs at least 30 generations (a launch-ahead loop from an idle GPU needs a few
+    # steps to fill: at 10 steps the fill and the final drain are ~10% of the wall time)
+    e2e_steps = max(args.steps, 30)
     barrier()
     t0 = time.perf_counter()
-    if os.environ.get("TEMO_E2E_PIPE", "0") == "1":  # host inputs drawn on a worker thread (opt-in)
-        stepper.start_host_pipeline(gen, args.steps)
-    for g in range(args.steps):
+    # NSGA-III host inputs drawn on a worker thread (large populations: the permutations take
+    # milliseconds; at pop 100 the thread hand-off costs more than it hides)
+    pipe = os.environ.get("TEMO_E2E_PIPE", "1") == "1" and c["pop"] * c["dim"] >= (1 << 20)
+    if pipe:
+        stepper.start_host_pipeline(gen, e2e_steps)
+    for g in range(e2e_steps):
         st, _ = stepper.step(st, g, gen, timed=False)  # host draws of step g+1 overlap step g on the GPU
         F_host[g % (LAG + 1)].copy_(stepper.objectives(st), non_blocking=True)
         done[g % (LAG + 1)].record()
         if g >= LAG:
             done[(g - LAG) % (LAG + 1)].synchronize()
-    for g in range(max(args.steps - LAG, 0), args.steps):
+    for g in range(max(e2e_steps - LAG, 0), e2e_steps):
         done[g % (LAG + 1)].synchronize()
     barrier()
-    e2e_value = args.steps / max_over_ranks(time.perf_counter() - t0)
+    e2e_value = e2e_steps / max_over_ranks(time.perf_counter() - t0)
     stepper.check()
     line = {
         "metric": c["metric"], "value": value, "unit": "gen/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args),
-        "e2e": {"value": e2e_value, "unit": "gen/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_value, "unit": "gen/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps, "host_pipeline": c["algorithm"] == "nsga3" and pipe},
         "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},
         "stages_note": "per-stage CUDA-event times from a separate serialised pass (randomness overlap off); "
                        "the timed region overlaps the next generation's randomness with this one's apply + selection",

@@ -442,7 +442,7 @@ double temo_probe_rows_rate(const double *X, const int64_t *pa, const int64_t *p
  * CUDA-event timing of each kernel stage on its own stream (off by default).
  * temo_timing_read syncs the recorded events, fills ms_out/calls_out
  * (TEMO_STAGE_COUNT entries each) and optionally resets the accumulators. */
-#define TEMO_STAGE_COUNT 15
+#define TEMO_STAGE_COUNT 16
 void temo_timing_enable(int on);
 const char *temo_timing_name(int stage);
 int temo_timing_read(double *ms_out, int64_t *calls_out, int reset);

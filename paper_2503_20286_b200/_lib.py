@@ -110,7 +110,7 @@ SIGNATURES = {
     "temo_timing_name": (ctypes.c_char_p, [_I32]),
     "temo_timing_read": (_I32, [_P, _P, _I32]),
 }
-STAGE_COUNT = 15
+STAGE_COUNT = 16
 
 TEMO_OK, TEMO_EINVAL, TEMO_ENAN, TEMO_ERUNTIME, TEMO_EWORKSPACE, TEMO_ECUDA = range(6)
 ST_NAN, ST_PEEL, ST_FILL, ST_DEMOTE, ST_COUNT, ST_KRANGE = 1, 2, 4, 8, 16, 32

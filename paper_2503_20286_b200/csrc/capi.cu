@@ -64,7 +64,7 @@ void stage_end(int stage, cudaStream_t st) {
 
 static const char *k_stage_names[TEMO_STAGE_COUNT] = {
     "rank_prep", "dom_bits", "peel", "normalize", "associate", "niche", "offspring",
-    "evaluate", "hv_count", "hv_contrib", "hype_select", "moead", "gather", "misc", "offspring_apply"};
+    "evaluate", "hv_count", "hv_contrib", "hype_select", "moead", "gather", "misc", "offspring_apply", "apply_vec"};
 
 extern "C" void temo_timing_enable(int on) {
     std::lock_guard<std::mutex> lk(temo::g_mu);

@@ -56,7 +56,8 @@ int num_sms();
 enum Stage {
     S_RANK_PREP = 0, S_DOM_BITS, S_PEEL, S_NORMALIZE, S_ASSOCIATE, S_NICHE, S_OFFSPRING,
     S_EVALUATE, S_HV_COUNT, S_HV_CONTRIB, S_HYPE_SELECT, S_MOEAD, S_GATHER, S_MISC,
-    S_OFFSPRING_APPLY  // the apply kernel of the two-phase offspring step (S_OFFSPRING: its randomness kernel)
+    S_OFFSPRING_APPLY,  // the apply stage of the two-phase offspring step (S_OFFSPRING: its randomness kernel)
+    S_APPLY_VEC         // the streaming kernel inside S_OFFSPRING_APPLY (k_offspring_apply_v)
 };
 void stage_begin(int stage, cudaStream_t st);
 void stage_end(int stage, cudaStream_t st);

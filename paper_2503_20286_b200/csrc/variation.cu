@@ -1875,6 +1875,7 @@ static __global__ void __launch_bounds__(256) k_pm_apply(VarArgs V, int64_t d, i
 // then the objectives from the apply kernel's sums plus the hit genes' terms.  A child whose
 // gene 0 was hit (the LSMOP linkage uses it for every gene) has its sums recomputed from its
 // row.  Children are bit-identical to the inline-PM kernels.
+constexpr int PMFIX_QS = 768;  // flag_stride(d) for d <= 3000
 template <int M, bool LSMOP>
 __global__ void __launch_bounds__(RW * 32, OFF_PMFIX_MINB) k_offspring_pm_fix(temo_problem P, VarArgs V, int64_t h, int64_t q0,
                                                               int64_t q1, const __grid_constant__ Philox ph,
@@ -1893,8 +1894,21 @@ __global__ void __launch_bounds__(RW * 32, OFF_PMFIX_MINB) k_offspring_pm_fix(te
     const int64_t avail = 4 - ph.pos;
     const double eta = V.eta_m + 1.0;
     const int64_t QP = quads_per_pair(d), QS = flag_stride(d);
-    for (int64_t q = q0 + (int64_t)blockIdx.x * RW + (threadIdx.x >> 5); q < q1; q += (int64_t)gridDim.x * RW) {
+    // the pair's flag row is staged in shared memory with 16-byte loads (one per lane for
+    // d <= 1020) instead of 32 lane-strided 2-byte loads per round; same gene order after
+    __shared__ __align__(16) uint16_t s_fl[RW][PMFIX_QS];
+    const bool staged = QS <= PMFIX_QS;
+    const int warp = threadIdx.x >> 5;
+    for (int64_t q = q0 + (int64_t)blockIdx.x * RW + warp; q < q1; q += (int64_t)gridDim.x * RW) {
         const uint16_t *fq = flags + q * QS;
+        if (staged) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(fq);
+            uint4 *dst = reinterpret_cast<uint4 *>(s_fl[warp]);
+            __syncwarp();  // every lane is done with the previous pair's row
+            for (int64_t v = lane; v < QS / 8; v += 32) dst[v] = __ldg(src + v);
+            __syncwarp();
+            fq = s_fl[warp];
+        }
         const int sh = (int)((o_mu + q * d - avail) & 3);
         double *orow[2] = {O + (dst_rows ? dst_rows[q] : q) * d, O + (dst_rows ? dst_rows[h + q] : h + q) * d};
         // gene 0 first (its final value enters every LSMOP term)
@@ -2520,12 +2534,14 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
         const int64_t items = (q1 - q0) * quads_per_pair(d);
         const unsigned gl = (unsigned)((items + 255) / 256 < num_sms() * 32 ? (items + 255) / 256 : num_sms() * 32);
         const unsigned gp = (unsigned)((pm_cap + 255) / 256 < num_sms() * 16 ? (pm_cap + 255) / 256 : num_sms() * 16);
+        stage_begin(S_APPLY_VEC, s);
         if (prob->id == TEMO_PROB_LSMOP1)
             k_offspring_apply_v<M, true><<<gv, RW * 32, sm_v, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
                                                                 gene_swap, beta, flags, O, FO, src_map, dst_rows);
         else
             k_offspring_apply_v<M, false><<<gv, RW * 32, sm_v, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
                                                                  gene_swap, beta, flags, O, FO, src_map, dst_rows);
+        stage_end(S_APPLY_VEC, s);
         k_pm_list<<<gl, 256, 0, s>>>(d, h, q0, q1, off, ph.pos, flags, pm_list, pm_cap);
         k_pm_apply<<<gp, 256, 0, s>>>(V, d, h, ph, off, gene_swap, pm_list, pm_cap, O, dst_rows);
         if (prob->id == TEMO_PROB_LSMOP1)
