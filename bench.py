@@ -593,6 +593,11 @@ def bench_run(args, c, dev, probes, barrier, max_over_ranks):
         "gpu_launches_per_step": launches,
         "clocks": clk,
     }
+    if c["algorithm"] == "nsga3" and os.environ.get("TEMO_BENCH_DROPIN", "1") == "1":
+        try:
+            line["dropin"] = bench_dropin(stepper, st, R, n, dev)
+        except Exception as exc:  # never lose the main line
+            line["dropin"] = {"error": repr(exc)}
     d = spec.d
     if c["algorithm"] in ("nsga3", "hype"):
         hbm, comp = roofline_offspring(n // 2, d, stages, args.steps, probes)
@@ -614,6 +619,31 @@ def bench_run(args, c, dev, probes, barrier, max_over_ranks):
         line["roofline"] = roofline_moead(n, d, m, T, ms / args.steps)
         line["launch_floor"] = launch_floor(dev, launches)
     return line
+
+
+def bench_dropin(stepper, st, R, n, dev):
+    """The reference-facing NumPy drop-in ``nsga3.environmental_selection(X, F, R, n, rng)``
+    (nsga3.py:186-218) on this generation's merged population as HOST arrays: X and F up, the
+    selection, the survivors' X and F down -- the call a reference user makes, PCIe included."""
+    import torch
+
+    from paper_2503_20286_b200.nsga3 import environmental_selection
+
+    N = stepper.N
+    Xh = st.rows(0, N).cpu().numpy()
+    Fh = st.cur.F[:N].cpu().numpy()
+    rng = np.random.Generator(np.random.Philox(7))
+    environmental_selection(Xh, Fh, R, n, rng)  # warm-up (workspaces)
+    torch.cuda.synchronize()
+    K = 3
+    t0 = time.perf_counter()
+    for _ in range(K):
+        Xn, Fn = environmental_selection(Xh, Fh, R, n, rng)
+    dt = (time.perf_counter() - t0) / K
+    return {"metric": "nsga3.environmental_selection calls/s (NumPy in, NumPy out)", "value": 1.0 / dt,
+            "ms_per_call": dt * 1e3, "h2d_bytes_per_call": Xh.nbytes + Fh.nbytes,
+            "d2h_bytes_per_call": Xn.nbytes + Fn.nbytes, "merged_N": N, "survivors": n,
+            "note": "pageable host arrays; dominated by the 3.2 GB X upload over PCIe"}
 
 
 def bench_ndsort(args, c, dev, probes, barrier, max_over_ranks):

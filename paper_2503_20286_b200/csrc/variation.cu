@@ -1103,6 +1103,9 @@ __global__ void __launch_bounds__(SW * 32, OFF_S_MINB) k_offspring_s(temo_proble
 #ifndef OFF_RAND_MINB
 #define OFF_RAND_MINB 4
 #endif
+#ifndef OFF_RAND_ONEGROUP
+#define OFF_RAND_ONEGROUP 1  // measured: rand 2.36 vs 2.39 ms at pop 200k (MINB 3: 2.43)
+#endif
 #ifndef OFF_APPLY_MINB
 #define OFF_APPLY_MINB 2
 #endif
@@ -1156,6 +1159,26 @@ __global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64
 #pragma unroll
             for (int k = 0; k < 4; ++k) okm |= (uint32_t)(gs + k >= 0 && gs + k < d) << k;
             uint32_t crossed = okm, negate = 0;
+#if OFF_RAND_ONEGROUP
+            // all streams of the quad in one lockstep group (more ILP, more registers)
+            constexpr int NS = SWAP ? 5 : 3;
+            uint64_t RA[NS][4];
+            {
+                int64_t E[NS];
+                if (SWAP) { E[0] = o_cross + es; E[1] = o_swap + es; }
+                E[NS - 3] = o_mu + es;
+                E[NS - 2] = o_hit + es;
+                E[NS - 1] = o_hit + hd + es;  // (unused in single mode)
+                raw_quads<NS>(ph, E, avail, RA);
+            }
+            if (SWAP) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    crossed &= ~((uint32_t)(RA[0][k] >> 63) << k);
+                    negate |= (uint32_t)(1u - (uint32_t)(RA[SWAP ? 1 : 0][k] >> 63)) << k;
+                }
+            }
+#else
             if (SWAP) {
                 uint64_t R[2][4];
                 const int64_t E[2] = {o_cross + es, o_swap + es};
@@ -1166,6 +1189,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64
                     negate |= (uint32_t)(1u - (uint32_t)(R[1][k] >> 63)) << k;
                 }
             }
+#endif
             const int nq = __popc(crossed);
             int incl = nq;
 #pragma unroll
@@ -1174,6 +1198,20 @@ __global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64
                 if (lane >= o) incl += y;
             }
             const int total = __shfl_sync(~0u, incl, 31);
+#if OFF_RAND_ONEGROUP
+            {
+                int slot = incl - nq;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if ((crossed >> k) & 1) s_mu[warp][slot++] = u01(RA[NS - 3][k]);
+            }
+            uint32_t hit = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                hit |= (uint32_t)(((okm >> k) & 1) && (int64_t)(RA[NS - 2][k] >> 11) <= pm_thr) << k;
+                if (!single) hit |= (uint32_t)(((okm >> k) & 1) && (int64_t)(RA[NS - 1][k] >> 11) <= pm_thr) << (4 + k);
+            }
+#else
             {
                 uint64_t R[1][4];
                 const int64_t E[1] = {o_mu + es};
@@ -1194,6 +1232,7 @@ __global__ void __launch_bounds__(RW * 32, OFF_RAND_MINB) k_offspring_rand(int64
                     if (!single) hit |= (uint32_t)(((okm >> k) & 1) && (int64_t)(R[1][k] >> 11) <= pm_thr) << (4 + k);
                 }
             }
+#endif
             if (j0 + lane < QP) flags[q * flag_stride(d) + j0 + lane] = (uint16_t)(crossed | hit << 4);
             __syncwarp();
             for (int t = lane; t < total; t += 32) s_mu[warp][t] = sbx_beta(s_mu[warp][t], e);
@@ -2372,6 +2411,19 @@ static bool offspring_s_disabled() {
 }
 
 // TEMO_APPLY_VEC=0 disables the vector gene-major apply kernel (d even, >= 128) (A/B)
+static bool apply_vec();
+// The PM hit list (k_pm_list) needs only the randomness phase's flags: it is built at the end of
+// temo_offspring_rand_ws (on the randomness stream, overlapped with the previous generation
+// when the harness runs the randomness ahead) instead of inside the apply stage.
+static bool pm_list_early(int64_t d) {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TEMO_PMLIST_EARLY");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v && d >= 128 && d % 2 == 0 && apply_vec();
+}
+
 static bool apply_vec() {
     static int v = -1;
     if (v < 0) {
@@ -2530,7 +2582,8 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
         const unsigned gf = (unsigned)wantf;
         // PM hits: compacted list (order irrelevant: each entry's result is fixed), one thread per
         // hit, then per pair the objectives from the apply sums + the hit genes' terms in gene order
-        TEMO_CUDA(cudaMemsetAsync(pm_list, 0, sizeof(int64_t), s));
+        const bool early = pm_list_early(d);
+        if (!early) TEMO_CUDA(cudaMemsetAsync(pm_list, 0, sizeof(int64_t), s));
         const int64_t items = (q1 - q0) * quads_per_pair(d);
         const unsigned gl = (unsigned)((items + 255) / 256 < num_sms() * 32 ? (items + 255) / 256 : num_sms() * 32);
         const unsigned gp = (unsigned)((pm_cap + 255) / 256 < num_sms() * 16 ? (pm_cap + 255) / 256 : num_sms() * 16);
@@ -2542,7 +2595,7 @@ int apply_m(const temo_problem *prob, const VarArgs &V, const double *X, const i
             k_offspring_apply_v<M, false><<<gv, RW * 32, sm_v, s>>>(*prob, V, X, i1, i2, h, q0, q1, ph, off,
                                                                  gene_swap, beta, flags, O, FO, src_map, dst_rows);
         stage_end(S_APPLY_VEC, s);
-        k_pm_list<<<gl, 256, 0, s>>>(d, h, q0, q1, off, ph.pos, flags, pm_list, pm_cap);
+        if (!early) k_pm_list<<<gl, 256, 0, s>>>(d, h, q0, q1, off, ph.pos, flags, pm_list, pm_cap);
         k_pm_apply<<<gp, 256, 0, s>>>(V, d, h, ph, off, gene_swap, pm_list, pm_cap, O, dst_rows);
         if (prob->id == TEMO_PROB_LSMOP1)
             k_offspring_pm_fix<M, true><<<gf, RW * 32, 0, s>>>(*prob, V, h, q0, q1, ph, off, gene_swap, flags, O, FO,
@@ -2811,6 +2864,16 @@ extern "C" int temo_offspring_rand_ws(const temo_variation *var, int64_t d, int6
         k_offspring_rand<true><<<grid, RW * 32, pad, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
     else
         k_offspring_rand<false><<<grid, RW * 32, pad, s>>>(d, V, h, q0, q1, ph, off, 0, beta, flags);
+    if (pm_list_early(d)) {
+        int64_t *pm_list = nullptr;
+        double *b2;
+        uint16_t *f2;
+        offspring_ws_split(ws, h, d, &b2, &f2, &pm_list);
+        const int64_t items = (q1 - q0) * quads_per_pair(d);
+        const unsigned gl = (unsigned)((items + 255) / 256 < num_sms() * 32 ? (items + 255) / 256 : num_sms() * 32);
+        TEMO_CUDA(cudaMemsetAsync(pm_list, 0, sizeof(int64_t), s));
+        k_pm_list<<<gl, 256, 0, s>>>(d, h, q0, q1, off, ph.pos, flags, pm_list, pm_list_cap(h, d));
+    }
     TEMO_LAUNCH_CHECK();
     stage_end(S_OFFSPRING, s);
     return TEMO_OK;
