@@ -673,7 +673,8 @@ def bench_ndsort(args, c, dev, probes, barrier, max_over_ranks):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    _lib.timing_enable(False)  # stage times come from the serialised pass below
+    _lib.timing_enable(True)
+    _lib.timing_read(reset=True)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -710,8 +711,6 @@ def bench_ndsort(args, c, dev, probes, barrier, max_over_ranks):
         "e2e": {"value": pairs / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": N * m * 8, "d2h_bytes_per_step": N * 4},
         "roofline": hbm, "roofline_compute": comp,
         "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items() if v[1]},
-        "stages_note": "per-stage CUDA-event times from a separate serialised pass (randomness overlap off); "
-                       "the timed region overlaps the next generation's randomness with this one's apply + selection",
         "gpu_launches": (launches * args.steps) if launches else None, "gpu_launches_per_step": launches,
         "clocks": clk,
     }
