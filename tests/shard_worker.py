@@ -25,6 +25,7 @@ def main():
     from paper_2503_20286_b200.harness import RunConfig, _resolve, _Stepper
     from paper_2503_20286_b200.rng import RngStream
 
+    predrawn = cfg.pop("predrawn", False)  # bench.py's loop: pre-drawn inputs, randomness overlap
     config = RunConfig(**cfg)
     config.validate()
     spec, R, n = _resolve(config)
@@ -33,8 +34,12 @@ def main():
     gen = RngStream(config.seed).split(0).generator()
     st = stepper.init(gen)
     ideals = []
+    pre = [None] * (config.generations + 2)
+    if predrawn:
+        pre = stepper.upload_host_inputs([stepper.draw_host_inputs(gen) for _ in range(config.generations)])
+        pre += [None, None]
     for g in range(1, config.generations + 1):
-        st, _ = stepper.step(st, g, gen, timed=False)
+        st, _ = stepper.step(st, g, gen, timed=False, pre=pre[g - 1], pre_next=pre[g])
         stepper.check()
         ideals.append(stepper.objectives(st).min(dim=0).values.cpu().numpy())
     X, F = stepper.population(st)

@@ -20,6 +20,9 @@ CASES = [
     dict(algorithm="nsga3", problem="dtlz2", objectives=3, pop_size=210, generations=4, seed=3),
     dict(algorithm="nsga3", problem="dtlz1", objectives=5, pop_size=126, generations=3, seed=4),
     dict(algorithm="nsga3", problem="lsmop1", objectives=3, pop_size=92, generations=2, seed=5),
+    # bench.py's sharded loop at a size with the randomness overlap on (n * D >= 2^20)
+    dict(algorithm="nsga3", problem="lsmop1", objectives=3, pop_size=1100, dim=1000, generations=3, seed=8,
+         predrawn=True),
     dict(algorithm="hype", problem="dtlz2", objectives=3, pop_size=64, generations=3, seed=6, hv_samples=140001),
     dict(algorithm="hype", problem="dtlz7", objectives=4, pop_size=50, generations=2, seed=7, hv_samples=70001),
 ]
