@@ -144,16 +144,24 @@ class MoeadEngine:
         n, T = self.n, self.T
         a = gen.integers(0, T, size=n)
         b = gen.integers(0, T - 1, size=n)
+        draws = DeviceDraws(gen)
+        off = draws.take(5 * n * self.spec.d if self.params.gene_swap else 3 * n * self.spec.d)
+        if self.graph and off == 0 and (n * self.spec.d) % 4 == 0 and self.spec.d <= 3000:
+            # the neighbour lookup I_nb[i, a_i], I_nb[i, b_i + (b_i >= a_i)] runs inside the graph:
+            # only the raw draws go up (2n int32 instead of the host fancy-indexing + 2n int64)
+            ab = np.empty(2 * n, dtype=np.int32)
+            ab[:n] = a
+            ab[n:] = b
+            if getattr(self, "_ab", None) is None:
+                self._ab = t.empty(2 * n, dtype=t.int32, device=self.dev)
+            self.ring.upload(ab, self._ab)
+            out = self._step_graph(st, draws)
+            draws.commit()
+            return out
         b = b + (b >= a)
         rows = np.arange(n)
         par = np.concatenate([self.I_nb_host[rows, a], self.I_nb_host[rows, b]]).astype(np.int64)
         self.ring.upload(par, self.parents)
-        draws = DeviceDraws(gen)
-        off = draws.take(5 * n * self.spec.d if self.params.gene_swap else 3 * n * self.spec.d)
-        if self.graph and off == 0 and (n * self.spec.d) % 4 == 0 and self.spec.d <= 3000:
-            out = self._step_graph(st, draws)
-            draws.commit()
-            return out
         L = _lib.lib()
         p = _lib.ptr
         rc = L.temo_moead_offspring(_lib.sptr(self.prob), _lib.sptr(self.var), p(st.X), p(self.parents),
@@ -188,6 +196,13 @@ class MoeadEngine:
         g = t.cuda.CUDAGraph()
         with t.cuda.graph(g, capture_error_mode="thread_local"):
             h = _lib.stream_handle(self.dev)
+            n = self.n
+            a = self._ab[:n].long()
+            b = self._ab[n:].long()
+            b = b + (b >= a).long()
+            rows = t.arange(n, device=self.dev)
+            self.parents[:n].copy_(self.I_nb[rows, a])
+            self.parents[n:].copy_(self.I_nb[rows, b])
             rc = L.temo_moead_offspring_dev(_lib.sptr(self.prob), _lib.sptr(self.var), ptr(gX[p]), ptr(self.parents),
                                             ptr(self.parents[self.n:]), self.n, ptr(st_dev), 0, ptr(self.O),
                                             ptr(self.F2), h)
