@@ -268,7 +268,9 @@ int temo_offspring_ws(const temo_problem *prob, const temo_variation *var, const
  * pair), so G ranks covering [0, h) together produce the full result bit for bit. */
 /* The two phases of temo_offspring_ws_range as separate calls (same workspace), so the
  * randomness of the next generation can run on a side stream while this generation's
- * selection runs (it needs no parent data).  Only when temo_offspring_two_phase(h, d). */
+ * selection runs (it needs no parent data).  Only when temo_offspring_two_phase(h, d).
+ * rand_ws writes the spread factors, the flags and (d even, >= 128) the PM hit list;
+ * apply_ws consumes them and must follow a rand_ws call with the same (h, q0, q1, st, off, ws). */
 int temo_offspring_two_phase(int64_t h, int64_t d);
 int temo_offspring_rand_ws(const temo_variation *var, int64_t d, int64_t h, int64_t q0, int64_t q1,
                            const temo_philox_state *st, uint64_t off, void *ws, size_t ws_bytes,
