@@ -596,7 +596,14 @@ class _Stepper:
                 self._pool_update(st, perm, keep)  # survivors' X rows stay where they are
                 _lib.gather_rows(self.selector.Fs, keep, nxt.F[:n])
             elif alg == "hype":  # no shuffle (hype.py:135-163)
-                keep = self.selector.select(cur.F, gen)
+                # launch-ahead loops (timed=False) defer the selection's RNG decision: the next
+                # generation's host draws were made from the speculatively advanced Generator;
+                # if the speculation was wrong, redo this generation's offspring from the
+                # restored state (children rows are rewritten; parents are untouched)
+                if self.selector.pending() and not self.selector.resolve():
+                    self._offspring(st, gen)
+                    cur = st.cur
+                keep = self.selector.select(cur.F, gen, defer=not timed)
                 self._pool_update(st, None, keep)
                 _lib.gather_rows(cur.F, keep, nxt.F[:n])
             else:  # rvea: apd_select over [parents; offspring] (rvea.py:33-68, harness.py:240-244)

@@ -145,7 +145,12 @@ class HypeSelector:
             lo, hi = self.col_bounds[r]
             self.Tseg = z((max(hi - lo, 1), N), dt=t.float64)
 
-    def select(self, F, rng, U=None):
+    def select(self, F, rng, U=None, defer: bool = False):
+        """``defer=True`` (launch-ahead loops): no host sync for the RNG decision -- the Generator
+        is advanced speculatively (the samples are drawn whenever the last front must be cut,
+        hype.py:154-158, i.e. almost always) and ``resolve()`` checks the device flag later,
+        undoing the advance if no samples were drawn."""
+        self.resolve()
         rank_device(F, self.n, SELECT, self.status, out=(self.rank, self.l, self.nf))
         L = _lib.lib()
         ws = _lib.workspace.get(self.ws_bytes, self.dev)
@@ -174,12 +179,38 @@ class HypeSelector:
                                         p(self.keep), p(self.v_hv), p(self.info), p(ws), ws.numel(), sh)
             _lib.check(rc, "hype.environmental_selection")
         self.info_host.copy_(self.info, non_blocking=True)
+        if defer and U is None:
+            t = _lib.torch()
+            ev = t.cuda.Event()
+            ev.record(t.cuda.current_stream(self.dev))
+            saved = rng.bit_generator.state
+            advance(rng, self.s * self.m)
+            self._pending = (ev, rng, saved)
+            return self.keep
         _lib.torch().cuda.current_stream(self.dev).synchronize()
         if U is None and int(self.info_host[3]):
             advance(rng, self.s * self.m)
         return self.keep
 
+    def pending(self) -> bool:
+        return getattr(self, "_pending", None) is not None
+
+    def resolve(self) -> bool:
+        """Settle a deferred RNG decision: True if the speculative advance was right (or nothing
+        was pending); False if it was undone (the Generator is back at the selection's end)."""
+        pend = getattr(self, "_pending", None)
+        if pend is None:
+            return True
+        ev, rng, saved = pend
+        self._pending = None
+        ev.synchronize()
+        if int(self.info_host[3]):
+            return True
+        rng.bit_generator.state = saved
+        return False
+
     def check(self):
+        self.resolve()
         _lib.sync_status(self.status, "hype.environmental_selection")
 
 

@@ -112,3 +112,42 @@ def test_config_c_golden_bit_exact(cuda):
     assert sel.info_host.numpy()[1] == int(z["k"])
     assert np.array_equal(sel.v_hv.cpu().numpy(), z["v_hv"])
     assert np.array_equal(keep, z["keep"])
+
+
+def test_deferred_rng_decision_equals_synced_loop(cuda):
+    """Launch-ahead loops (step(timed=False)) advance the Generator speculatively after each HypE
+    selection and settle the device's drew-samples flag one generation later, redoing the
+    offspring when no samples were drawn; populations and the final Generator state equal the
+    synced loop's.  Small populations make exact front fits (no samples drawn) frequent, so the
+    undo path runs."""
+    import json
+
+    import torch
+
+    from paper_2503_20286_b200.harness import RunConfig, _resolve, _Stepper
+    from paper_2503_20286_b200.rng import RngStream
+
+    undone = 0
+    for seed, pop in ((1, 6), (2, 8), (3, 10), (4, 12)):
+        cfg = RunConfig(algorithm="hype", problem="dtlz2", objectives=2, dim=6, pop_size=pop, seed=seed,
+                        hv_samples=1001)
+        spec, R, n = _resolve(cfg)
+        outs = []
+        for timed in (True, False):
+            st_ = _Stepper(cfg, spec, R, n)
+            gen = RngStream(seed).split(0).generator()
+            st = st_.init(gen)
+            flags = []
+            for g in range(12):
+                st, _ = st_.step(st, g, gen, timed=timed)
+                if timed:
+                    flags.append(int(st_.selector.info_host[3]))
+            st_.check()
+            X, F = st_.population(st)
+            outs.append((X.cpu().numpy(), F.cpu().numpy(),
+                         json.dumps(gen.bit_generator.state, default=lambda a: np.asarray(a).tolist())))
+            if timed:
+                undone += flags.count(0)
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1]), (seed, pop)
+        assert outs[0][2] == outs[1][2], (seed, pop)
+    assert undone > 0, "no generation exercised the undo path"
