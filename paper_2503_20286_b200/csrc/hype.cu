@@ -26,33 +26,37 @@ constexpr int SAMPLE_BLOCK = 65536;  // hype.py:58
 constexpr int SUB = 2048;          // dgemv_t sub-block (App. A7)
 
 // ---------------------------------------------------------------- alpha
-__global__ void k_alpha(int64_t n1, int64_t k, double *__restrict__ alpha) {
-    if (threadIdx.x || blockIdx.x) return;
-    // lam[0] = 1, lam[l] = (k - l) / (n1 - l); alpha[c] = cumprod(lam)[c] / (c + 1)
-    double c = 1.0;
-    for (int64_t q = 0; q < n1; ++q) {
-        if (q < k) {
+// alpha[c] = cumprod(lam)[c] / (c + 1) with lam[0] = 1, lam[l] = (k - l) / (n1 - l) (hype.py:24-33,
+// np.cumprod: a sequential product).  Thread 0 runs the product chain in order and stops once it
+// is exactly 0.0 (every later product is 0 too -- bit-exact) or at q = k; the CTA zero-fills the
+// rest in parallel.  One CTA of ALPHA_T threads.
+constexpr int ALPHA_T = 256;
+__device__ __forceinline__ void alpha_body(int64_t n1, int64_t k, double *__restrict__ alpha) {
+    __shared__ int64_t s_stop;
+    if (threadIdx.x == 0) {
+        double c = 1.0;
+        int64_t q = 0;
+        const int64_t qk = k < n1 ? k : n1;
+        for (; q < qk; ++q) {
             if (q > 0) c = c * ((double)(k - q) / (double)(n1 - q));
+            if (c == 0.0) break;
             alpha[q] = c / (double)(q + 1);
-        } else {
-            alpha[q] = 0.0;
         }
+        s_stop = q;
     }
+    __syncthreads();
+    for (int64_t q = s_stop + threadIdx.x; q < n1; q += blockDim.x) alpha[q] = 0.0;
+}
+
+__global__ void __launch_bounds__(ALPHA_T) k_alpha(int64_t n1, int64_t k, double *__restrict__ alpha) {
+    alpha_body(n1, k, alpha);
 }
 
 // alpha from the device-side k (scal[1]); only when estimation runs (scal[2])
-__global__ void k_alpha_dev(int64_t n1, const int32_t *__restrict__ scal, double *__restrict__ alpha) {
-    if (threadIdx.x || blockIdx.x || !scal[2]) return;
-    const int64_t k = scal[1];
-    double c = 1.0;
-    for (int64_t q = 0; q < n1; ++q) {
-        if (q < k) {
-            if (q > 0) c = c * ((double)(k - q) / (double)(n1 - q));
-            alpha[q] = c / (double)(q + 1);
-        } else {
-            alpha[q] = 0.0;
-        }
-    }
+__global__ void __launch_bounds__(ALPHA_T) k_alpha_dev(int64_t n1, const int32_t *__restrict__ scal,
+                                                       double *__restrict__ alpha) {
+    if (!scal[2]) return;
+    alpha_body(n1, scal[1], alpha);
 }
 
 // ---------------------------------------------------------------- column stats
@@ -484,7 +488,7 @@ using namespace temo;
 
 extern "C" int temo_hype_alpha(int64_t n1, int64_t k, double *alpha, temo_stream_t stream) {
     if (n1 < 1 || k < 1 || k > n1 || !alpha) return TEMO_EINVAL;
-    k_alpha<<<1, 1, 0, (cudaStream_t)stream>>>(n1, k, alpha);
+    k_alpha<<<1, ALPHA_T, 0, (cudaStream_t)stream>>>(n1, k, alpha);
     TEMO_LAUNCH_CHECK();
     return TEMO_OK;
 }
@@ -523,7 +527,7 @@ extern "C" int temo_hv_estimate(const double *F, int64_t n1, int m, const double
     plan_hv(p, nullptr, n1, m, s);
     if (!ws || ws_bytes < p.total) return TEMO_EWORKSPACE;
     plan_hv(p, ws, n1, m, s);
-    k_alpha<<<1, 1, 0, sm>>>(n1, k, p.alpha);
+    k_alpha<<<1, ALPHA_T, 0, sm>>>(n1, k, p.alpha);
     const int32_t one = 1;
     TEMO_CUDA(cudaMemcpyAsync(p.ok, &one, sizeof(int32_t), cudaMemcpyHostToDevice, sm));
     const int rc = hv_run(p, F, v_ref, st, off, U, v_hv, sm);
@@ -575,7 +579,7 @@ extern "C" int temo_hype_select_begin(const double *F, int64_t N, int m, int64_t
     k_hype_k<<<gdim(N), 256, 0, sm>>>(rank, l, N, n, w.a.scal);
     k_hype_k_final<<<1, 1, 0, sm>>>(w.a.scal, n, w.h.ok);  // estimation only if k >= 1 (hype.py:156)
     stage_end(S_HYPE_SELECT, sm);
-    k_alpha_dev<<<1, 1, 0, sm>>>(N, w.a.scal, w.h.alpha);
+    k_alpha_dev<<<1, ALPHA_T, 0, sm>>>(N, w.a.scal, w.h.alpha);
     hv_prepare(w.h, F, v_ref, sm);
     TEMO_LAUNCH_CHECK();
     return TEMO_OK;
