@@ -548,6 +548,58 @@ class _Stepper:
         caller.wait_stream(self._hp)
         return out
 
+    def _sel_graph_on(self) -> bool:
+        """Small NSGA-III populations are host-launch bound (~50 launches per selection): the
+        selection (shuffle gather, ND sort, normalize/associate/niche, pool update, survivor
+        objectives) is replayed as one CUDA graph per buffer parity.  TEMO_SEL_GRAPH=0: off."""
+        import os
+
+        if getattr(self, "_sel_graph_env", None) is None:
+            self._sel_graph_env = os.environ.get("TEMO_SEL_GRAPH", "1") != "0"
+        return (self._sel_graph_env and self.config.algorithm == "nsga3" and self.shard is None
+                and self.N <= 16384 and getattr(self.selector, "dist_rank", None) is None)
+
+    def _select_graph(self, st: DeviceState, perm):
+        """The NSGA-III selection of this generation as a graph replay.  The graph is keyed by
+        the buffers it touches (current/next objective buffers and row maps alternate with
+        period 2); the shuffle goes to the fixed ``self.perm`` first.  The first use of a key
+        runs eagerly (workspaces settle), the second captures."""
+        t = _lib.torch()
+        if perm.data_ptr() != self.perm.data_ptr():
+            self.perm.copy_(perm)
+        cur, nxt, n = st.cur, st.nxt, self.n
+        out = self.phys[1] if st.phys.data_ptr() == self.phys[0].data_ptr() else self.phys[0]
+        key = (cur.F.data_ptr(), nxt.F.data_ptr(), st.phys.data_ptr())
+        graphs = self.__dict__.setdefault("_sel_graphs", {})
+        seen = self.__dict__.setdefault("_sel_seen", set())
+
+        def body():
+            keep = self.selector.select(cur.F, self.perm)
+            self._pool_update(st, self.perm, keep)
+            _lib.gather_rows(self.selector.Fs, keep, nxt.F[:n])
+
+        g = graphs.get(key)
+        if g is None and key in seen:
+            g = t.cuda.CUDAGraph()
+            phys_in = st.phys
+            try:
+                with t.cuda.graph(g, capture_error_mode="thread_local"):
+                    body()
+            except Exception:  # capture not possible here: eager from now on (nothing ran)
+                self._sel_graph_env = False
+                g = None
+                t.cuda.synchronize(self.dev)
+            st.phys = phys_in  # capture does not run the work: replay below (or eager)
+            if g is not None:
+                graphs[key] = g
+        if g is None:
+            seen.add(key)
+            body()
+            return
+        g.replay()
+        st.phys = out
+        st.extra["pool_identity"] = False
+
     def _overlap_on(self) -> bool:
         """The randomness overlap pays off only when the randomness is large: at small populations
         the extra stream hand-offs cost more host time than they hide (pop 100: 1.6 vs 1.7 kgen/s)."""
@@ -592,9 +644,12 @@ class _Stepper:
                     perm = self.ring.upload(rng_permutation(gen, self.N), self.perm)
                 else:
                     perm = pre.shuffle
-                keep = self.selector.select(cur.F, perm)
-                self._pool_update(st, perm, keep)  # survivors' X rows stay where they are
-                _lib.gather_rows(self.selector.Fs, keep, nxt.F[:n])
+                if self._sel_graph_on():
+                    self._select_graph(st, perm)
+                else:
+                    keep = self.selector.select(cur.F, perm)
+                    self._pool_update(st, perm, keep)  # survivors' X rows stay where they are
+                    _lib.gather_rows(self.selector.Fs, keep, nxt.F[:n])
             elif alg == "hype":  # no shuffle (hype.py:135-163)
                 # launch-ahead loops (timed=False) defer the selection's RNG decision: the next
                 # generation's host draws were made from the speculatively advanced Generator;

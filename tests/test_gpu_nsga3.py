@@ -329,3 +329,37 @@ def test_selection_vs_oracle_workload_scale(cuda, N, kind):
     k = int(sel.counts[0].item())
     assert np.array_equal(sel.promoted[:k].cpu().numpy(), want["promoted"])
     assert np.array_equal(keep, want["keep"])
+
+
+@pytest.mark.parametrize("m,pop,problem", [(3, 100, "dtlz1"), (5, 210, "dtlz2"), (3, 2000, "lsmop1")])
+def test_selection_graph_equals_eager_loop(cuda, m, pop, problem, monkeypatch):
+    """The small-population NSGA-III selection replayed as a CUDA graph (one per buffer parity)
+    gives the eager loop's populations, every generation's ideal point and Generator state."""
+    import json
+
+    import torch
+
+    from paper_2503_20286_b200.harness import RunConfig, _resolve, _Stepper
+    from paper_2503_20286_b200.rng import RngStream
+
+    cfg = RunConfig(algorithm="nsga3", problem=problem, objectives=m, dim=30 if problem == "lsmop1" else None,
+                    pop_size=pop, seed=11)
+    spec, R, n = _resolve(cfg)
+    outs = []
+    for on in ("0", "1"):
+        monkeypatch.setenv("TEMO_SEL_GRAPH", on)
+        st_ = _Stepper(cfg, spec, R, n)
+        gen = RngStream(11).split(0).generator()
+        st = st_.init(gen)
+        ideals = []
+        for g in range(8):
+            st, _ = st_.step(st, g, gen, timed=(g % 3 == 0))
+            ideals.append(st_.objectives(st).min(dim=0).values.cpu().numpy())
+        st_.check()
+        if on == "1":
+            assert len(getattr(st_, "_sel_graphs", {})) == 2, "selection graphs were not captured"
+        X, F = st_.population(st)
+        outs.append((X.cpu().numpy(), F.cpu().numpy(), np.asarray(ideals),
+                     json.dumps(gen.bit_generator.state, default=lambda a: np.asarray(a).tolist())))
+    for a, b in zip(outs[0], outs[1]):
+        assert (a == b) if isinstance(a, str) else np.array_equal(a, b)
